@@ -1,0 +1,112 @@
+"""50-digit mpmath evaluations used to pin the oracle (test-only).
+
+Written from PAPER.md directly, in a different arrangement from the oracle
+where one exists, so a transcription slip in either shows up:
+
+* s-factors, eqs. (14)-(16) and s#
+* I0, I2, eqs. (18)-(19)
+* brute-force per-delta sums of eqs. (10)-(13).  The
+  stresslet uses the equivalent arrangement
+      T^d_iac = -6 [ s3 yh_i yh_a yh_c / r^5 + (s2 - s3) t1_iac / r^3 ]
+  which follows from eq. (7) with t2 = yh yh yh - b^2 t1 (expand
+  yh = b n0 - xh); the oracle uses the t1/t2 form literally.
+"""
+from __future__ import annotations
+
+import mpmath as mp
+
+mp.mp.dps = 50
+SQPI = mp.sqrt(mp.pi)
+
+
+def s_factors(t):
+    t = mp.mpf(t)
+    E = mp.erf(t)
+    G = 2 / SQPI * mp.exp(-t * t)
+    return E, E - G * t, E - G * (t + mp.mpf(2) / 3 * t ** 3)
+
+
+def s_sharp(t):
+    t = mp.mpf(t)
+    E = mp.erf(t)
+    e = mp.exp(-t * t)
+    return (E + 2 / (3 * SQPI) * (5 * t - 2 * t ** 3) * e,
+            E - 2 / (3 * SQPI) * (3 * t - 14 * t ** 3 + 4 * t ** 5) * e,
+            E - 2 / (9 * SQPI) * (9 * t + 6 * t ** 3 - 4 * t ** 5) * e)
+
+
+def I0(lam):
+    lam = mp.mpf(lam)
+    a = abs(lam)
+    return mp.exp(-lam ** 2) / SQPI - a * mp.erfc(a)
+
+
+def I2(lam):
+    lam = mp.mpf(lam)
+    a = abs(lam)
+    return mp.mpf(2) / 3 * ((mp.mpf(1) / 2 - lam ** 2) * mp.exp(-lam ** 2) / SQPI + a ** 3 * mp.erfc(a))
+
+
+def _reg(r, d):
+    """(s1/r, s2/r^3, s3/r^5) with the exact r -> 0 limits."""
+    if r == 0:
+        return 2 / (SQPI * d), 4 / (3 * SQPI * d ** 3), 8 / (15 * SQPI * d ** 5)
+    s1, s2, s3 = s_factors(r / d)
+    return s1 / r, s2 / r ** 3, s3 / r ** 5
+
+
+def brute_deltas(block, targets, mode=3):
+    """Definition-mode u^dk, v^dk at 50 digits for the listed target indices.
+    Returns dict k -> (u list[3][T], v list[3][T]) as mpf."""
+    N = block.N
+    X = [[mp.mpf(float(block.src_xyz[i, s])) for s in range(N)] for i in range(3)]
+    Nn = [[mp.mpf(float(block.src_normal[i, s])) for s in range(N)] for i in range(3)]
+    W = [mp.mpf(float(w)) for w in block.src_weight]
+    Fd = [[mp.mpf(float(block.f[i, s])) for s in range(N)] for i in range(3)]
+    Qd = [[mp.mpf(float(block.q[i, s])) for s in range(N)] for i in range(3)]
+    deltas = [mp.mpf(r) * mp.mpf(block.h) for r in block.rho]
+    out = {k: ([[None] * len(targets) for _ in range(3)], [[None] * len(targets) for _ in range(3)])
+           for k in range(3)}
+    for ti, t in enumerate(targets):
+        y = [mp.mpf(float(block.tgt_xyz[i, t])) for i in range(3)]
+        b = mp.mpf(float(block.tgt_b[t]))
+        n0 = [mp.mpf(float(block.tgt_x0_density[i, t])) for i in range(3)]
+        f0 = [mp.mpf(float(block.tgt_x0_density[3 + i, t])) for i in range(3)]
+        q0 = [mp.mpf(float(block.tgt_x0_density[6 + i, t])) for i in range(3)]
+        x0 = [y[i] - b * n0[i] for i in range(3)]
+        alpha = sum(f0[i] * n0[i] for i in range(3))
+        chi = mp.mpf(1) if b < 0 else (mp.mpf(0) if b > 0 else mp.mpf(1) / 2)
+        U = [[mp.mpf(0)] * 3 for _ in range(3)]
+        V = [[mp.mpf(0)] * 3 for _ in range(3)]
+        for s in range(N):
+            yh = [y[i] - X[i][s] for i in range(3)]
+            xh = [X[i][s] - x0[i] for i in range(3)]
+            m = [Nn[i][s] for i in range(3)]
+            r = mp.sqrt(sum(c * c for c in yh))
+            g = [Fd[a][s] - alpha * m[a] for a in range(3)]
+            dq = [Qd[a][s] - q0[a] for a in range(3)]
+            yg = sum(yh[a] * g[a] for a in range(3))
+            yq = sum(yh[a] * dq[a] for a in range(3))
+            ym = sum(yh[c] * m[c] for c in range(3))
+            # t1 contracted with dq_a m_c (eq. 8)
+            nq = sum(n0[a] * dq[a] for a in range(3))
+            nm = sum(n0[c] * m[c] for c in range(3))
+            xq = sum(xh[a] * dq[a] for a in range(3))
+            xm = sum(xh[c] * m[c] for c in range(3))
+            t1c = [b * n0[i] * nq * nm - (xh[i] * nq * nm + n0[i] * xq * nm + n0[i] * nq * xm) for i in range(3)]
+            for k, d in enumerate(deltas):
+                if r == 0:
+                    A1, A3, A5 = _reg(r, d)
+                    s2ms3_r3 = 4 / (3 * SQPI * d ** 3)
+                else:
+                    s1, s2, s3 = s_factors(r / d)
+                    A1, A3, A5 = s1 / r, s2 / r ** 3, s3 / r ** 5
+                    s2ms3_r3 = (s2 - s3) / r ** 3
+                for i in range(3):
+                    U[k][i] += W[s] * (g[i] * A1 + yh[i] * yg * A3)
+                    V[k][i] += W[s] * (-6) * (A5 * yh[i] * yq * ym + s2ms3_r3 * t1c[i])
+        for k in range(3):
+            for i in range(3):
+                out[k][0][i][ti] = U[k][i] / (8 * mp.pi)
+                out[k][1][i][ti] = V[k][i] / (8 * mp.pi) + chi * q0[i]
+    return out
