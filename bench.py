@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path (BASELINE.json metric).
+
+One step = one stokes_er_eval (SL+DL, 3-delta localized regularization with the
+fused extrapolation) over BASELINE.json configs[1] at 1/h = 64: the unit
+sphere's N = 68,166 quadrature nodes as sources, M = 102,249 targets (all nodes
+at b = 0 plus N/2 shell targets, b ~ U[-3h, 3h]), rho = (2,3,4), seeded cubic
+densities.  Inputs are resident in HBM when the timed region starts; L2 is
+flushed (256 MiB write) between timed steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  Multi-GPU (torchrun): targets are independent
+(PAPER.md:167-169), so every rank evaluates its own seeded instance of the
+workload with no data-path collective ("weak" scaling); value = all ranks'
+pairs / max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "target-source pair interactions/sec (SL+DL, 3-delta extrap) & FP64 % of peak"
+UNIT = "pairs/s"
+# Stated per-pair FLOP counts: algorithmic
+# flops with rsqrt/erf/exp = 1; FMA = 2.
+F_FAR_ALG = 57
+F_NEAR_ALG = 180
+F_FAR_ISSUED = 64   # ncu-countable FP64 flops (2*DFMA + DMUL + DADD) of far_pair<3> (41 instructions)
+SMS = 148
+FP64_LANES_PER_SM = 64  # measured: DFMA loop 58.7 FMA/clk/SM at the boost clock (tools/probes)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based); default configs[1]")
+    ap.add_argument("--inv-h", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--targets-per-thread", type=int, default=0)
+    return ap.parse_args()
+
+
+def make_workload(cfg: int, inv_h: int, rank: int):
+    from workloads.configs import config1, config2, config3, config5
+    seed = cfg + 1000 * rank
+    if cfg == 1:
+        return config1(seed=seed)
+    if cfg == 2:
+        return config2(inv_h=inv_h, seed=seed)
+    if cfg == 3:
+        return config3(inv_h=inv_h, seed=seed)
+    if cfg == 5:
+        return config5(inv_h=inv_h, seed=seed)
+    raise SystemExit("bench configs: 1, 2, 3, 5 (config 4 is a 4-block parity case)")
+
+
+def near_pair_count(block) -> int:
+    """Pairs with r <= 6 delta_max (the near rule of include/stokes_er.h), by KD-tree."""
+    from scipy.spatial import cKDTree
+    rc = 6.0 * max(block.rho) * block.h
+    return int(cKDTree(block.tgt_xyz.T).count_neighbors(cKDTree(block.src_xyz.T), rc))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (localized mode = the paper's algorithm) as it
+    stands, on the host cores, rank 0 only; each step a bounded target sample."""
+    if rank != 0:
+        return None
+    import oracle
+    block = make_workload(args.config, args.inv_h, 0)
+    cores = oracle.max_threads()
+    rng = np.random.default_rng(0)
+    k = 256
+    t0 = time.perf_counter()
+    oracle.evaluate_block(block.take_targets(rng.choice(block.M, k, replace=False)), localized=True)
+    per_target = (time.perf_counter() - t0) / k
+    k = int(min(block.M, max(64, 0.4 / per_target)))  # ~0.4 s per step
+    times, pairs = [], 0
+    for it in range(args.warmup + args.steps):
+        idx = rng.choice(block.M, k, replace=False)
+        sub = block.take_targets(idx)
+        t0 = time.perf_counter()
+        oracle.evaluate_block(sub, localized=True)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            pairs += k * block.N
+    total = sum(times)
+    value = pairs / total
+    cpu = {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{k} random targets of {block.M} per step x all {block.N} sources, localized mode "
+                     f"(shared far field, PAPER.md:183-191), {args.steps} steps"}
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": block.name, "N": block.N, "M": block.M, "h": block.h, "rho": list(block.rho)},
+            "cpu_baseline": cpu, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0}}
+
+
+def cpu_baseline(block):
+    """The oracle (localized) on the host cores, bounded sample of ~10 s of CPU work."""
+    import oracle
+    cores = oracle.max_threads()
+    rng = np.random.default_rng(1)
+    k = 256
+    t0 = time.perf_counter()
+    oracle.evaluate_block(block.take_targets(rng.choice(block.M, k, replace=False)), localized=True)
+    per_target = (time.perf_counter() - t0) / k
+    k = int(min(block.M, max(256, 10.0 / per_target)))
+    idx = rng.choice(block.M, k, replace=False)
+    t0 = time.perf_counter()
+    oracle.evaluate_block(block.take_targets(idx), localized=True)
+    dt = time.perf_counter() - t0
+    return {"value": k * block.N / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{k} random targets of {block.M} x all {block.N} sources, localized mode "
+                      f"(paper's shared-far-field algorithm), {dt:.1f} s wall"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2507_00156_b200 as ser
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+
+    block = make_workload(args.config, args.inv_h, rank)
+    M, N = block.M, block.N
+    pairs = M * N
+    near = near_pair_count(block)
+    arrs = ser.to_device(block, dev)
+    out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+    opt = ser.Options()
+    if args.targets_per_thread:
+        opt.targets_per_thread = args.targets_per_thread
+    nbytes = int(ser._lib.load().stokes_er_workspace_bytes_ex(M, N, 3, __import__("ctypes").byref(opt)))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    K, W = args.steps, args.warmup
+
+    def step(ev_pair=None):
+        if ev_pair is not None:
+            opt.pair_kernel_start_event = ev_pair[0].cuda_event
+            opt.pair_kernel_end_event = ev_pair[1].cuda_event
+        else:
+            opt.pair_kernel_start_event = None
+            opt.pair_kernel_end_event = None
+        ser.evaluate(*arrs, block.h, block.rho, out_u=out_u, out_v=out_v, workspace=ws, stream=stream,
+                     options=opt)
+
+    for _ in range(W):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    evp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for a, b in evp:  # torch creates the CUDA event lazily on first record: materialize the handles
+        a.record(stream)
+        b.record(stream)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            flush.zero_()  # L2 flush, outside the timed events
+            ev[i][0].record(stream)
+            step(evp[i])
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    pair_ms = [a.elapsed_time(b) for a, b in evp]
+    total_s = sum(step_ms) / 1e3
+    if dist is not None:
+        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+    value = world * pairs * K / total_s
+
+    # end-to-end through the C ABI with pinned HOST buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.from_numpy(a).pin_memory() for a in block.arrays()]
+        hu = torch.empty((3, M), dtype=torch.float64).pin_memory()
+        hv = torch.empty((3, M), dtype=torch.float64).pin_memory()
+        hws = ser.alloc_workspace(M, N, 3, dev, host=True)
+        for _ in range(2):
+            ser.evaluate_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws, stream=stream)
+        ke = max(3, K // 4)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e_ms = []
+        for _ in range(ke):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ser.evaluate_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws, stream=stream)
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        e_total = sum(e_ms) / 1e3
+        if dist is not None:
+            t = torch.tensor([e_total], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_total = float(t.item())
+        e2e = {"value": world * pairs * ke / e_total, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(a.nbytes for a in block.arrays())),
+               "d2h_bytes_per_step": int(hu.numel() * 8 + hv.numel() * 8)}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    clocks = clk.summary()
+    pair_avg_s = statistics.mean(pair_ms) / 1e3
+    far = pairs - near
+    alg_flops = far * F_FAR_ALG + near * F_NEAR_ALG
+    f_clk = 1965.0
+    peak = SMS * FP64_LANES_PER_SM * 2 * f_clk * 1e6 / 1e12  # TFLOP/s
+    achieved = alg_flops / pair_avg_s / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None,
+                "kernel": "pair_kernel<3,2> (FP64 pipe)",
+                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM (DFMA-loop probe) x 2 x 1965 MHz max SM clock",
+                "flops_per_launch": alg_flops, "flop_convention": f"far {F_FAR_ALG}, near {F_NEAR_ALG} algorithmic",
+                "far_issued_frac": (far * F_FAR_ISSUED + near * F_NEAR_ALG) / pair_avg_s / 1e12 / peak,
+                "pair_kernel_ms": pair_avg_s * 1e3,
+                "pair_kernel_share": sum(pair_ms) / sum(step_ms)}
+    if clocks.get("sm_mhz"):
+        roofline["frac_at_measured_clock"] = achieved / (SMS * FP64_LANES_PER_SM * 2 * clocks["sm_mhz"] / 1e6)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": block.name, "N": N, "M": M, "pairs_per_step": pairs, "near_pairs_per_step": near,
+                       "h": block.h, "rho": list(block.rho), "mode": "SL+DL", "cutoff": 6.0,
+                       "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM",
+                       "targets_per_thread": int(opt.stats[3]), "work_items": int(opt.stats[0]),
+                       "grid_ctas": int(opt.stats[1]), "chunk_tiles": int(opt.stats[2]),
+                       "parallelism": f"target-sharded x{world} (independent instances)"},
+            "fp64_tflops_alg": alg_flops * K * world / total_s / 1e12,
+            "roofline": roofline, "clocks": clocks,
+            "gpu_launches": K * ser.launch_count(M, N, 3),
+            "gpu_launches_note": "our kernels per step: bbox, 2 morton, pack_sources, pack_targets, pair, finalize "
+                                 "(+ CUB radix-sort launches, library code)",
+            "e2e": e2e}
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(block)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * stokes_er.h -- C ABI of the B200 (sm_100a) hot path of the localized
+ * extrapolated-regularization method for nearly singular Stokes layer
+ * potentials (PAPER.md = arXiv 2507.00156, LaTeX source).
+ *
+ * One call evaluates, for M targets y near a closed surface discretized by N
+ * quadrature nodes x (weights w, unit outward normals n), the subtracted,
+ * regularized single layer (Stokeslet, eq. (10) `Stokes_SL2`)
+ * and double layer (stresslet, eq. (11) `Stokes_DL2`)
+ *
+ *   u^d_i(y) = 1/(8pi) sum_x S^d_ij(y,x) [f_j(x) - (f(x0).n0) n_j(x)] w(x)
+ *   v^d_i(y) = 1/(8pi) sum_x T^d_ijk(y,x) [q_j(x) - q_j(x0)] n_k(x) w(x) + chi(y) q_i(x0)
+ *
+ * with S^d, T^d of eqs. (12)-(13) (split of eq. (7),
+ * PAPER.md:59-69) and smoothing factors s1, s2, s3 of eqs. (14)-(16)
+ * (PAPER.md:90-102), for delta_k = rho_k h, k = 1..3, and
+ * returns the extrapolated value: the u of the 3x3 system eq. (17)
+ * with I0, I2 of eqs. (18)-(19),
+ * lambda_k = b/delta_k; the same system for v.
+ *
+ * The regularization is localized: a pair (y, x) is NEAR
+ * iff |y - x|^2 <= (STOKES_ER_CUTOFF * max_k delta_k)^2; near pairs use
+ * s_i(r/delta_k) for all three delta_k, far pairs use the unregularized S
+ * (eq. 3) and T (eq. 4) once, shared by the three sums (eq. (26) `near_far`).
+ *
+ * Conventions for every entry point below
+ *  - All arrays are FP64, "SoA row-major": a [R][C] array stores row r at
+ *    offset r*C.  Pointers are DEVICE pointers unless the name says _host.
+ *    8-byte alignment is required.  The library never frees or keeps them.
+ *  - Targets: y = x0 + b n0 with |n0| = 1, b the signed distance (> 0
+ *    outside), x0 the closest surface point.  The library trusts
+ *    this consistency; it does no projection.  chi = 1, 1/2, 0 for b < 0,
+ *    b == 0, b > 0.
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *    default stream).  Device entry points only ENQUEUE work and return; the
+ *    caller synchronizes.  No global mutable state: calls on different
+ *    streams with different workspaces may run concurrently.
+ *  - Workspace: caller-owned device memory of at least
+ *    stokes_er_workspace_bytes(M, N, mode) bytes, 256-byte aligned; its
+ *    contents need no initialization and are garbage afterwards.
+ *  - Errors: a non-zero stokes_er_status is returned and NOTHING is enqueued
+ *    when host-side validation fails (EINVAL, EWORKSPACE, EARCH).  ECUDA is
+ *    returned if a CUDA call or launch fails (outputs then undefined).
+ */
+#ifndef STOKES_ER_H
+#define STOKES_ER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STOKES_ER_ABI_VERSION 1
+/* c: near iff r <= c * max(delta_k)  ("s1=s2=s3=1 for t > 6") */
+#define STOKES_ER_CUTOFF 6.0
+
+typedef enum {
+  STOKES_ER_SL = 1,   /* single layer only: f required, out_u written            */
+  STOKES_ER_DL = 2,   /* double layer only: q required, out_v written            */
+  STOKES_ER_BOTH = 3  /* both                                                    */
+} stokes_er_mode;
+
+typedef enum {
+  STOKES_ER_OK = 0,
+  STOKES_ER_EINVAL = 1,     /* NULL pointer required by mode, M < 0, N < 1, h <= 0 or not
+                               finite, rho not positive strictly increasing, bad mode   */
+  STOKES_ER_ECUDA = 2,      /* a CUDA runtime call or kernel launch failed              */
+  STOKES_ER_EWORKSPACE = 3, /* workspace NULL or smaller than stokes_er_workspace_bytes */
+  STOKES_ER_EARCH = 4       /* current device is not compute capability 10.x (sm_100)   */
+} stokes_er_status;
+
+/* Bytes of device workspace needed by stokes_er_eval / stokes_er_eval_deltas. */
+size_t stokes_er_workspace_bytes(int64_t M, int64_t N, int mode);
+
+/*
+ * The hot path.  Inputs (device, FP64):
+ *   src_xyz        [3][N]  quadrature nodes x
+ *   src_normal     [3][N]  unit outward normals n(x)
+ *   src_weight     [N]     quadrature weights w(x) >= 0          (eq. (23))
+ *   f              [3][N]  SL density at the nodes   (may be NULL if mode == DL)
+ *   q              [3][N]  DL density at the nodes   (may be NULL if mode == SL)
+ *   tgt_xyz        [3][M]  targets y
+ *   tgt_b          [M]     signed distance b
+ *   tgt_x0_density [9][M]  rows 0-2: n0 = n(x0); rows 3-5: f(x0); rows 6-8: q(x0)
+ *                          (f/q rows ignored when the mode does not use them)
+ *   M >= 0 (M == 0: returns OK, enqueues nothing), N >= 1, h > 0,
+ *   rho[3] HOST array, 0 < rho_1 < rho_2 < rho_3 (equal rho make eq. (17) singular)
+ * Outputs (device, FP64, fully overwritten):
+ *   out_u [3][M] extrapolated SL velocity u (with the 1/(8pi))   (NULL if mode == DL)
+ *   out_v [3][M] extrapolated DL velocity v incl. chi q(x0)       (NULL if mode == SL)
+ */
+int stokes_er_eval(const double* src_xyz, const double* src_normal, const double* src_weight,
+                   const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                   const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
+                   int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
+/*
+ * Same as stokes_er_eval with HOST input/output buffers (pinned memory
+ * recommended): enqueues the host->device copies of the inputs into the
+ * workspace, the evaluation, and the device->host copies of out_u / out_v,
+ * then SYNCHRONIZES `stream` (the host outputs are valid on return).
+ * Workspace: stokes_er_host_workspace_bytes(M, N, mode) device bytes.
+ */
+size_t stokes_er_host_workspace_bytes(int64_t M, int64_t N, int mode);
+int stokes_er_eval_host(const double* src_xyz_host, const double* src_normal_host,
+                        const double* src_weight_host, const double* f_host, const double* q_host,
+                        const double* tgt_xyz_host, const double* tgt_b_host,
+                        const double* tgt_x0_density_host, int64_t M, int64_t N, double h,
+                        const double rho[3], int mode, double* out_u_host, double* out_v_host,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Debug / test entry point: the three per-delta values u^{delta_k}, v^{delta_k}
+ * of eqs. (10)-(11) (incl. 1/(8pi) and chi q(x0)), same localized near/far
+ * rule, no extrapolation.  out_udelta, out_vdelta: [3][3][M] = [k][i][m].
+ * A simple one-target-per-thread kernel (not the tuned path).
+ */
+int stokes_er_eval_deltas(const double* src_xyz, const double* src_normal, const double* src_weight,
+                          const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                          const double* tgt_x0_density, int64_t M, int64_t N, double h,
+                          const double rho[3], int mode, double* out_udelta, double* out_vdelta,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * The extrapolation solve alone (eq. (17)): for each target m and column c,
+ * out[c][m] = u solving  u + c1 rho_k I0(b/delta_k) + c2 rho_k^3 I2(b/delta_k) = in[k][c][m].
+ * in_delta [3][C][M] device, out [C][M] device, tgt_b [M] device, 1 <= C <= 64.
+ * Targets with |b| > STOKES_ER_CUTOFF * delta_3 (no near pairs, all u^{delta_k}
+ * equal) and numerically singular systems return in[0][c][m] (R7).
+ */
+int stokes_er_extrapolate(const double* tgt_b, int64_t M, double h, const double rho[3],
+                          const double* in_delta, int C, double* out, void* stream);
+
+/* Number of kernel launches one stokes_er_eval(M, N, mode) enqueues. */
+int stokes_er_launch_count(int64_t M, int64_t N, int mode);
+
+/* Optional profiling hooks for bench.py: if non-NULL, cudaEvent_t handles
+ * (as void*) recorded on `stream` immediately before / after the pair-sum
+ * kernel (the dominant kernel) of the NEXT stokes_er_eval_ex call. */
+typedef struct {
+  void* pair_kernel_start_event;
+  void* pair_kernel_end_event;
+  int targets_per_thread; /* 0 = default; 2 or 4 (tuning/tests)          */
+  int source_chunk_tiles; /* 0 = automatic; work item = chunk * 128 sources */
+  int64_t stats[4];       /* out: [0] work items, [1] grid CTAs, [2] chunk tiles, [3] targets/thread */
+} stokes_er_options;
+
+/* Workspace for stokes_er_eval_ex with these tuning options (>= stokes_er_workspace_bytes
+ * when the options force a finer source chunking). */
+size_t stokes_er_workspace_bytes_ex(int64_t M, int64_t N, int mode, const stokes_er_options* options);
+
+int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const double* src_weight,
+                      const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                      const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
+                      int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
+                      void* stream, stokes_er_options* options);
+
+const char* stokes_er_status_string(int status);
+int stokes_er_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STOKES_ER_H */

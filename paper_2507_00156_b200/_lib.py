@@ -1,0 +1,82 @@
+"""ctypes binding of include/stokes_er.h (argument marshalling only).
+
+Every step of the evaluation runs in libstokes_er.so's CUDA kernels.  There is
+no CPU fallback: a missing library or a missing GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libstokes_er.so")
+
+STATUS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "EWORKSPACE", 4: "EARCH"}
+
+_dp = ctypes.c_void_p  # device or host pointers are passed as raw addresses
+_i64 = ctypes.c_int64
+
+
+class StokesERError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn} failed: status {status} ({STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("pair_kernel_start_event", ctypes.c_void_p), ("pair_kernel_end_event", ctypes.c_void_p),
+                ("targets_per_thread", ctypes.c_int), ("source_chunk_tiles", ctypes.c_int),
+                ("stats", ctypes.c_int64 * 4)]
+
+
+EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_er_eval", "stokes_er_eval_ex", "stokes_er_host_workspace_bytes",
+           "stokes_er_eval_host", "stokes_er_eval_deltas", "stokes_er_extrapolate", "stokes_er_launch_count",
+           "stokes_er_status_string", "stokes_er_abi_version"]
+
+_lib = None
+
+
+def load():
+    """Load libstokes_er.so (built by paper_2507_00156_b200.build / __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: the CUDA extension is not built "
+                          "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    eval_args = [_dp] * 8 + [_i64, _i64, ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                             _dp, _dp, _dp, ctypes.c_size_t, _dp]
+    L.stokes_er_workspace_bytes.argtypes = [_i64, _i64, ctypes.c_int]
+    L.stokes_er_workspace_bytes.restype = ctypes.c_size_t
+    L.stokes_er_workspace_bytes_ex.argtypes = [_i64, _i64, ctypes.c_int, ctypes.POINTER(Options)]
+    L.stokes_er_workspace_bytes_ex.restype = ctypes.c_size_t
+    L.stokes_er_host_workspace_bytes.argtypes = [_i64, _i64, ctypes.c_int]
+    L.stokes_er_host_workspace_bytes.restype = ctypes.c_size_t
+    L.stokes_er_eval.argtypes = eval_args
+    L.stokes_er_eval.restype = ctypes.c_int
+    L.stokes_er_eval_ex.argtypes = eval_args + [ctypes.POINTER(Options)]
+    L.stokes_er_eval_ex.restype = ctypes.c_int
+    L.stokes_er_eval_host.argtypes = eval_args
+    L.stokes_er_eval_host.restype = ctypes.c_int
+    L.stokes_er_eval_deltas.argtypes = eval_args
+    L.stokes_er_eval_deltas.restype = ctypes.c_int
+    L.stokes_er_extrapolate.argtypes = [_dp, _i64, ctypes.c_double, ctypes.POINTER(ctypes.c_double), _dp,
+                                        ctypes.c_int, _dp, _dp]
+    L.stokes_er_extrapolate.restype = ctypes.c_int
+    L.stokes_er_launch_count.argtypes = [_i64, _i64, ctypes.c_int]
+    L.stokes_er_launch_count.restype = ctypes.c_int
+    L.stokes_er_status_string.argtypes = [ctypes.c_int]
+    L.stokes_er_status_string.restype = ctypes.c_char_p
+    L.stokes_er_abi_version.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(fn: str, status: int):
+    if status != 0:
+        raise StokesERError(fn, status, load().stokes_er_status_string(status).decode())
+
+
+def rho_arg(rho):
+    return (ctypes.c_double * 3)(*[float(r) for r in rho])

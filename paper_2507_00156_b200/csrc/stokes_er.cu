@@ -1,0 +1,462 @@
+// stokes_er.cu -- the C ABI of include/stokes_er.h: argument validation,
+// workspace planning, launches on the caller's stream; plus the two small
+// test entry points (per-delta sums, the extrapolation solve alone).
+#include <algorithm>
+#include <climits>
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace ser {
+
+// ------------------------------------------- debug: per-delta sums (simple)
+// One target per thread over the raw (unsorted) inputs; same near/far rule
+// and the same pair algebra as K1 but one accumulator set per delta_k.
+template <int MODE>
+__global__ void deltas_kernel(const double* __restrict__ sx, const double* __restrict__ sn,
+                              const double* __restrict__ sw, const double* __restrict__ f,
+                              const double* __restrict__ q, const double* __restrict__ ty,
+                              const double* __restrict__ tb, const double* __restrict__ x0d, int64_t M,
+                              int64_t N, double h, Delta3 rho, double rc2, double r2_tiny,
+                              double* __restrict__ out_ud, double* __restrict__ out_vd) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const double y[3] = {ty[i], ty[M + i], ty[2 * M + i]};
+  const double b = tb[i];
+  double n0[3], f0[3], q0[3];
+  for (int d = 0; d < 3; ++d) {
+    n0[d] = x0d[d * M + i];
+    f0[d] = (MODE & 1) ? x0d[(3 + d) * M + i] : 0.0;
+    q0[d] = (MODE & 2) ? x0d[(6 + d) * M + i] : 0.0;
+  }
+  const double alpha = f0[0] * n0[0] + f0[1] * n0[1] + f0[2] * n0[2];
+  double inv_delta[3];
+  for (int k = 0; k < 3; ++k) inv_delta[k] = 1.0 / (rho.rho[k] * h);
+  double Uf[3] = {0, 0, 0}, Vf[3] = {0, 0, 0}, U[3][3] = {}, V[3][3] = {};
+  for (int64_t s = 0; s < N; ++s) {
+    const double w = sw[s];
+    double d[3], m[3], g[3], dq[3];
+    for (int c = 0; c < 3; ++c) {
+      d[c] = y[c] - sx[c * N + s];
+      m[c] = sn[c * N + s] * w;
+      g[c] = (MODE & 1) ? f[c * N + s] * w - alpha * m[c] : 0.0;
+      dq[c] = (MODE & 2) ? q[c * N + s] - q0[c] : 0.0;
+    }
+    const double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+    const double dg = d[0] * g[0] + d[1] * g[1] + d[2] * g[2];
+    const double dqq = d[0] * dq[0] + d[1] * dq[1] + d[2] * dq[2];
+    const double dm = d[0] * m[0] + d[1] * m[1] + d[2] * m[2];
+    if (r2 > rc2) {
+      const double ri = 1.0 / sqrt(r2);
+      const double ri3 = ri * ri * ri, ri5 = ri3 * ri * ri;
+      for (int c = 0; c < 3; ++c) {
+        Uf[c] += g[c] * ri + d[c] * dg * ri3;
+        Vf[c] += d[c] * dqq * dm * ri5;
+      }
+      continue;
+    }
+    double xh[3];
+    for (int c = 0; c < 3; ++c) xh[c] = b * n0[c] - d[c];
+    const double an = n0[0] * dq[0] + n0[1] * dq[1] + n0[2] * dq[2];
+    const double cn = n0[0] * m[0] + n0[1] * m[1] + n0[2] * m[2];
+    const double dd = xh[0] * dq[0] + xh[1] * dq[1] + xh[2] * dq[2];
+    const double e = xh[0] * m[0] + xh[1] * m[1] + xh[2] * m[2];
+    double P[3];
+    for (int c = 0; c < 3; ++c) P[c] = n0[c] * (b * an * cn - dd * cn - an * e) - xh[c] * an * cn;
+    for (int k = 0; k < 3; ++k) {
+      double A1, A3, A5, AP;
+      if (r2 < r2_tiny) {
+        const double id = inv_delta[k];
+        A1 = kTwoOverSqrtPi * id;
+        A3 = (2.0 / 3.0) * kTwoOverSqrtPi * id * id * id;
+        A5 = (4.0 / 15.0) * kTwoOverSqrtPi * id * id * id * id * id;
+        AP = A3;
+      } else {
+        const double r = sqrt(r2);
+        double s1, s2, s3, c23;
+        s_factors(r * inv_delta[k], s1, s2, s3, c23);
+        A1 = s1 / r;
+        A3 = s2 / (r2 * r);
+        A5 = s3 / (r2 * r2 * r);
+        AP = c23 / (r2 * r);
+      }
+      for (int c = 0; c < 3; ++c) {
+        U[k][c] += g[c] * A1 + d[c] * dg * A3;
+        V[k][c] += d[c] * dqq * dm * A5 + P[c] * AP;
+      }
+    }
+  }
+  const double inv8pi = 1.0 / (8.0 * kPi);
+  const double chi = b < 0.0 ? 1.0 : (b > 0.0 ? 0.0 : 0.5);
+  for (int k = 0; k < 3; ++k)
+    for (int c = 0; c < 3; ++c) {
+      if (MODE & 1) out_ud[(k * 3 + c) * M + i] = (Uf[c] + U[k][c]) * inv8pi;
+      if (MODE & 2) out_vd[(k * 3 + c) * M + i] = -6.0 * (Vf[c] + V[k][c]) * inv8pi + chi * q0[c];
+    }
+}
+
+// ------------------------------------------- the extrapolation solve alone
+__global__ void extrapolate_kernel(const double* __restrict__ tb, int64_t M, double h, Delta3 rho,
+                                   const double* __restrict__ in, int C, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  double w[3];
+  extrap_weights(tb[i], h, rho.rho, STOKES_ER_CUTOFF, w);
+  for (int c = 0; c < C; ++c) {
+    const double a0 = in[((int64_t)0 * C + c) * M + i], a1 = in[((int64_t)1 * C + c) * M + i],
+                 a2 = in[((int64_t)2 * C + c) * M + i];
+    out[(int64_t)c * M + i] = (w[1] == 0.0 && w[2] == 0.0) ? a0 : fma(w[0], a0, fma(w[1], a1, w[2] * a2));
+  }
+}
+
+}  // namespace ser
+
+// =================================================================== host side
+namespace {
+
+using namespace ser;
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct Plan {
+  int mode = 3, T = 2;
+  int64_t M = 0, N = 0, Mpad = 0, Npad = 0;
+  int n_tiles = 0, n_tblocks = 0, chunk_tiles = 0, n_chunks = 0, n_items = 0;
+  size_t cub_bytes = 0;
+  size_t off_box, off_skin, off_skout, off_svin, off_svout, off_tkin, off_tkout, off_tvin, off_tvout;
+  size_t off_cub, off_src, off_srcbox, off_tgt, off_orig, off_partial, off_counter, total;
+};
+
+size_t cub_sort_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+                                  static_cast<int32_t*>(nullptr), static_cast<int>(n), 0, 30);
+  return bytes;
+}
+
+Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override) {
+  Plan p;
+  p.mode = mode;
+  p.T = (T == 4) ? 4 : 2;
+  p.M = M;
+  p.N = N;
+  p.Npad = ceil_div(N, kTile) * kTile;
+  p.n_tiles = static_cast<int>(p.Npad / kTile);
+  const int TB = kThreads * p.T;
+  p.n_tblocks = static_cast<int>(ceil_div(M > 0 ? M : 1, TB));
+  p.Mpad = (int64_t)p.n_tblocks * TB;
+  // work items (target block, source chunk): >= 16 per nominal CTA slot so the
+  // dynamic queue's tail is small, each >= 4 tiles, partials <= 256 MB.
+  int64_t want = ceil_div(16 * kNominalCtas, p.n_tblocks);
+  const int64_t mem_cap = std::max<int64_t>(1, (int64_t)(kPartialCapBytes / (48.0 * (double)p.Mpad)));
+  const int64_t max_chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.n_tiles, 4), mem_cap));
+  want = std::min<int64_t>(std::max<int64_t>(want, 1), max_chunks);
+  p.chunk_tiles = static_cast<int>(ceil_div(p.n_tiles, want));
+  if (chunk_override > 0) p.chunk_tiles = std::min(chunk_override, p.n_tiles);
+  p.n_chunks = static_cast<int>(ceil_div(p.n_tiles, p.chunk_tiles));
+  p.n_items = p.n_tblocks * p.n_chunks;
+  p.cub_bytes = std::max(cub_sort_bytes(N), cub_sort_bytes(std::max<int64_t>(M, 1)));
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  p.off_box = take(8 * sizeof(double));
+  p.off_skin = take(N * 4);
+  p.off_skout = take(N * 4);
+  p.off_svin = take(N * 4);
+  p.off_svout = take(N * 4);
+  p.off_tkin = take(M * 4);
+  p.off_tkout = take(M * 4);
+  p.off_tvin = take(M * 4);
+  p.off_tvout = take(M * 4);
+  p.off_cub = take(p.cub_bytes);
+  p.off_src = take(p.Npad * kSrcDoubles * sizeof(double));
+  p.off_srcbox = take((p.Npad / kSub) * 8 * sizeof(double));
+  p.off_tgt = take(p.Mpad * kTgtFields * sizeof(double));
+  p.off_orig = take(p.Mpad * sizeof(int32_t));
+  p.off_partial = take((size_t)p.n_items * 6 * TB * sizeof(double));
+  p.off_counter = take(sizeof(int) * 4);
+  p.total = off;
+  return p;
+}
+
+bool rho_ok(const double* rho) {
+  return rho && std::isfinite(rho[0]) && std::isfinite(rho[2]) && rho[0] > 0.0 && rho[1] > rho[0] &&
+         rho[2] > rho[1];
+}
+
+int validate(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
+             const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
+             const double* rho, int mode) {
+  if (mode < 1 || mode > 3) return STOKES_ER_EINVAL;
+  if (M < 0 || N < 1 || M > INT32_MAX || N > INT32_MAX) return STOKES_ER_EINVAL;
+  if (!(h > 0.0) || !std::isfinite(h) || !rho_ok(rho)) return STOKES_ER_EINVAL;
+  if (!sx || !sn || !sw) return STOKES_ER_EINVAL;
+  if (M > 0 && (!ty || !tb || !x0d)) return STOKES_ER_EINVAL;  // M == 0: no target arrays needed
+  if ((mode & 1) && !f) return STOKES_ER_EINVAL;
+  if ((mode & 2) && !q) return STOKES_ER_EINVAL;
+  return STOKES_ER_OK;
+}
+
+int check_arch() {
+  int dev = 0, major = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return STOKES_ER_ECUDA;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  return major == 10 ? STOKES_ER_OK : STOKES_ER_EARCH;
+}
+
+template <int MODE, int T>
+void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<MODE, T>, kThreads, 0);
+  const int grid = std::max(1, std::min(pp.n_items, sms * std::max(occ, 1)));
+  *grid_out = grid;
+  pair_kernel<MODE, T><<<grid, kThreads, 0, s>>>(pp);
+}
+
+template <int MODE>
+int run_eval(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
+             const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
+             const double* rho, double* out_u, double* out_v, char* ws, const Plan& P, cudaStream_t s,
+             stokes_er_options* opt) {
+  double* box = reinterpret_cast<double*>(ws + P.off_box);
+  uint32_t* skin = reinterpret_cast<uint32_t*>(ws + P.off_skin);
+  uint32_t* skout = reinterpret_cast<uint32_t*>(ws + P.off_skout);
+  int32_t* svin = reinterpret_cast<int32_t*>(ws + P.off_svin);
+  int32_t* svout = reinterpret_cast<int32_t*>(ws + P.off_svout);
+  uint32_t* tkin = reinterpret_cast<uint32_t*>(ws + P.off_tkin);
+  uint32_t* tkout = reinterpret_cast<uint32_t*>(ws + P.off_tkout);
+  int32_t* tvin = reinterpret_cast<int32_t*>(ws + P.off_tvin);
+  int32_t* tvout = reinterpret_cast<int32_t*>(ws + P.off_tvout);
+  double* src = reinterpret_cast<double*>(ws + P.off_src);
+  double* srcbox = reinterpret_cast<double*>(ws + P.off_srcbox);
+  double* tgt = reinterpret_cast<double*>(ws + P.off_tgt);
+  int32_t* orig = reinterpret_cast<int32_t*>(ws + P.off_orig);
+  double* partial = reinterpret_cast<double*>(ws + P.off_partial);
+  int* counter = reinterpret_cast<int*>(ws + P.off_counter);
+
+  bbox_kernel<<<1, 1024, 0, s>>>(sx, N, ty, M, box);
+  morton_kernel<<<ceil_div(N, 256), 256, 0, s>>>(sx, N, box, skin, svin);
+  morton_kernel<<<ceil_div(M, 256), 256, 0, s>>>(ty, M, box, tkin, tvin);
+  size_t cb = P.cub_bytes;
+  if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, skin, skout, svin, svout, (int)N, 0, 30, s) !=
+      cudaSuccess)
+    return STOKES_ER_ECUDA;
+  cb = P.cub_bytes;
+  if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, tkin, tkout, tvin, tvout, (int)M, 0, 30, s) !=
+      cudaSuccess)
+    return STOKES_ER_ECUDA;
+  pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox);
+  Delta3 r3{{rho[0], rho[1], rho[2]}};
+  pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, tgt, orig);
+  if (cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
+
+  PairParams pp;
+  pp.src = src;
+  pp.src_box = srcbox;
+  pp.tgt = tgt;
+  pp.partial = partial;
+  pp.counter = counter;
+  pp.Mpad = P.Mpad;
+  pp.n_items = P.n_items;
+  pp.n_chunks = P.n_chunks;
+  pp.chunk_tiles = P.chunk_tiles;
+  pp.n_tiles = P.n_tiles;
+  const double dmax = rho[2] * h;
+  pp.rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  pp.rc2_box = pp.rc2 * (1.0 + 1e-9);
+  pp.r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
+  for (int k = 0; k < 3; ++k) pp.inv_delta[k] = 1.0 / (rho[k] * h);
+
+  if (opt && opt->pair_kernel_start_event)
+    cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
+  int grid = 0;
+  if (P.T == 4) launch_pairs<MODE, 4>(pp, s, &grid);
+  else launch_pairs<MODE, 2>(pp, s, &grid);
+  if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
+  if (opt) {
+    opt->stats[0] = P.n_items;
+    opt->stats[1] = grid;
+    opt->stats[2] = P.chunk_tiles;
+    opt->stats[3] = P.T;
+  }
+  finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, tgt, orig, M, P.Mpad, P.n_chunks,
+                                                          kThreads * P.T, out_u, out_v);
+  return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+int opt_T(const stokes_er_options* o) { return (o && o->targets_per_thread == 4) ? 4 : 2; }
+int opt_chunk(const stokes_er_options* o) { return o ? o->source_chunk_tiles : 0; }
+
+size_t host_stage_bytes(int64_t M, int64_t N) {
+  return align_up(13 * N * sizeof(double)) + align_up(13 * M * sizeof(double)) + align_up(6 * M * sizeof(double)) +
+         4 * kAlign;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t stokes_er_workspace_bytes(int64_t M, int64_t N, int mode) {
+  if (M < 0 || N < 1 || mode < 1 || mode > 3) return 0;
+  // the larger of the two tunings, so one workspace serves every option
+  return std::max(make_plan(M, N, mode, 2, 0).total, make_plan(M, N, mode, 4, 0).total);
+}
+
+size_t stokes_er_workspace_bytes_ex(int64_t M, int64_t N, int mode, const stokes_er_options* options) {
+  if (M < 0 || N < 1 || mode < 1 || mode > 3) return 0;
+  return std::max(stokes_er_workspace_bytes(M, N, mode),
+                  make_plan(M, N, mode, opt_T(options), opt_chunk(options)).total);
+}
+
+int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const double* src_weight,
+                      const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                      const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
+                      int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
+                      void* stream, stokes_er_options* options) {
+  int st = validate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode);
+  if (st) return st;
+  if (M == 0) return STOKES_ER_OK;
+  if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
+  if ((st = check_arch())) return st;
+  const Plan P = make_plan(M, N, mode, opt_T(options), opt_chunk(options));
+  if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  switch (mode) {
+    case 1:
+      return run_eval<1>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho,
+                         out_u, out_v, ws, P, s, options);
+    case 2:
+      return run_eval<2>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho,
+                         out_u, out_v, ws, P, s, options);
+    default:
+      return run_eval<3>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho,
+                         out_u, out_v, ws, P, s, options);
+  }
+}
+
+int stokes_er_eval(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
+                   const double* q, const double* tgt_xyz, const double* tgt_b, const double* tgt_x0_density,
+                   int64_t M, int64_t N, double h, const double rho[3], int mode, double* out_u, double* out_v,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  return stokes_er_eval_ex(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho,
+                           mode, out_u, out_v, workspace, workspace_bytes, stream, nullptr);
+}
+
+size_t stokes_er_host_workspace_bytes(int64_t M, int64_t N, int mode) {
+  const size_t w = stokes_er_workspace_bytes(M, N, mode);
+  return w ? align_up(w) + host_stage_bytes(M, N) : 0;
+}
+
+int stokes_er_eval_host(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
+                        const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
+                        const double rho[3], int mode, double* out_u, double* out_v, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  int st = validate(sx, sn, sw, f, q, ty, tb, x0d, M, N, h, rho, mode);
+  if (st) return st;
+  if (M == 0) return STOKES_ER_OK;
+  if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
+  if ((st = check_arch())) return st;
+  const size_t wbytes = align_up(stokes_er_workspace_bytes(M, N, mode));
+  if (!workspace || workspace_bytes < wbytes + host_stage_bytes(M, N)) return STOKES_ER_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* stage = static_cast<char*>(workspace) + wbytes;
+  double* dsx = reinterpret_cast<double*>(stage);
+  double *dsn = dsx + 3 * N, *dsw = dsn + 3 * N, *df = dsw + N, *dq = df + 3 * N;
+  double* dty = reinterpret_cast<double*>(stage + align_up(13 * N * sizeof(double)));
+  double *dtb = dty + 3 * M, *dx0 = dtb + M;
+  double* du =
+      reinterpret_cast<double*>(stage + align_up(13 * N * sizeof(double)) + align_up(13 * M * sizeof(double)));
+  double* dv = du + 3 * M;
+  auto h2d = [&](double* dst, const double* src, int64_t n) {
+    return src ? cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, s) : cudaSuccess;
+  };
+  if (h2d(dsx, sx, 3 * N) || h2d(dsn, sn, 3 * N) || h2d(dsw, sw, N) || h2d(df, (mode & 1) ? f : nullptr, 3 * N) ||
+      h2d(dq, (mode & 2) ? q : nullptr, 3 * N) || h2d(dty, ty, 3 * M) || h2d(dtb, tb, M) || h2d(dx0, x0d, 9 * M))
+    return STOKES_ER_ECUDA;
+  st = stokes_er_eval_ex(dsx, dsn, dsw, (mode & 1) ? df : nullptr, (mode & 2) ? dq : nullptr, dty, dtb, dx0, M, N,
+                         h, rho, mode, (mode & 1) ? du : nullptr, (mode & 2) ? dv : nullptr, workspace, wbytes,
+                         stream, nullptr);
+  if (st) return st;
+  if ((mode & 1) && cudaMemcpyAsync(out_u, du, 3 * M * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  if ((mode & 2) && cudaMemcpyAsync(out_v, dv, 3 * M * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  return cudaStreamSynchronize(s) == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+int stokes_er_eval_deltas(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
+                          const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
+                          const double rho[3], int mode, double* out_ud, double* out_vd, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  int st = validate(sx, sn, sw, f, q, ty, tb, x0d, M, N, h, rho, mode);
+  if (st) return st;
+  if (M == 0) return STOKES_ER_OK;
+  if (((mode & 1) && !out_ud) || ((mode & 2) && !out_vd)) return STOKES_ER_EINVAL;
+  if ((st = check_arch())) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Delta3 r3{{rho[0], rho[1], rho[2]}};
+  const double dmax = rho[2] * h;
+  const double rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  const double r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
+  const int grid = static_cast<int>(ceil_div(M, 128));
+  switch (mode) {
+    case 1:
+      deltas_kernel<1><<<grid, 128, 0, s>>>(sx, sn, sw, f, q, ty, tb, x0d, M, N, h, r3, rc2, r2_tiny, out_ud, out_vd);
+      break;
+    case 2:
+      deltas_kernel<2><<<grid, 128, 0, s>>>(sx, sn, sw, f, q, ty, tb, x0d, M, N, h, r3, rc2, r2_tiny, out_ud, out_vd);
+      break;
+    default:
+      deltas_kernel<3><<<grid, 128, 0, s>>>(sx, sn, sw, f, q, ty, tb, x0d, M, N, h, r3, rc2, r2_tiny, out_ud, out_vd);
+  }
+  return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+int stokes_er_extrapolate(const double* tgt_b, int64_t M, double h, const double rho[3], const double* in_delta,
+                          int C, double* out, void* stream) {
+  if (M < 0 || M > INT32_MAX || !(h > 0.0) || !std::isfinite(h) || !rho_ok(rho) || C < 1 || C > 64)
+    return STOKES_ER_EINVAL;
+  if (!tgt_b || !in_delta || !out) return STOKES_ER_EINVAL;
+  if (M == 0) return STOKES_ER_OK;
+  const int st = check_arch();
+  if (st) return st;
+  Delta3 r3{{rho[0], rho[1], rho[2]}};
+  extrapolate_kernel<<<ceil_div(M, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tgt_b, M, h, r3, in_delta,
+                                                                                       C, out);
+  return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+int stokes_er_launch_count(int64_t M, int64_t N, int mode) {
+  (void)N;
+  (void)mode;
+  // bbox, 2x morton, pack sources, pack targets, pair, finalize: our kernels.
+  // The two CUB radix sorts add their own launches (library code).
+  return M > 0 ? 7 : 0;
+}
+
+const char* stokes_er_status_string(int status) {
+  switch (status) {
+    case STOKES_ER_OK: return "ok";
+    case STOKES_ER_EINVAL: return "invalid argument";
+    case STOKES_ER_ECUDA: return "CUDA error";
+    case STOKES_ER_EWORKSPACE: return "workspace too small";
+    case STOKES_ER_EARCH: return "device is not sm_100 (B200)";
+    default: return "unknown status";
+  }
+}
+
+int stokes_er_abi_version(void) { return STOKES_ER_ABI_VERSION; }
+
+}  // extern "C"

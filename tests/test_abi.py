@@ -1,0 +1,65 @@
+"""The C-ABI library loads and exports every symbol include/stokes_er.h declares (CPU only: no compute calls)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "stokes_er.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(stokes_er_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2507_00156_b200 import build
+    build.build()
+    from paper_2507_00156_b200 import _lib
+    return _lib.load()
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for n in ["stokes_er_eval", "stokes_er_workspace_bytes", "stokes_er_eval_deltas", "stokes_er_extrapolate",
+              "stokes_er_eval_host", "stokes_er_status_string"]:
+        assert n in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_2507_00156_b200 import _lib
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert set(_lib.EXPORTS) == set(declared_functions())
+
+
+def test_pure_host_queries(lib):
+    assert lib.stokes_er_abi_version() == 1
+    assert lib.stokes_er_status_string(3) == b"workspace too small"
+    assert lib.stokes_er_launch_count(0, 10, 3) == 0
+
+
+def test_sm100a_only_cubin():
+    """The library carries sm_100a SASS (no PTX JIT fallback for other archs)."""
+    import subprocess
+    from paper_2507_00156_b200 import build
+    path = build.build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass or "UBLKPF" in sass or "BLKCP" in sass  # TMA bulk copy in the pair kernel
+    assert "DFMA" in sass and "MUFU.RSQ64H" in sass
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2507_00156_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, fn)).read()
+                assert "import oracle" not in text and "from oracle" not in text and "liboracle" not in text, fn

@@ -1,0 +1,220 @@
+"""GPU parity: the sm_100a path through the C ABI vs the CPU oracle (-m gpu).
+
+Tolerance (BASELINE.json north_star): max-norm relative error
+    max_i |gpu_i - oracle_i| / max_i |oracle_i|  <= 1e-12
+separately for u and v, and <= 1e-13 for the extrapolation solve alone.
+The oracle runs in definition mode (every pair regularized) unless noted; the
+GPU path localizes, which moves totals by <= 6e-16 relative.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads.configs import config1, config2, config3, config4, config5, subsample
+from workloads.densities import ConstField, RigidField
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+TOL_SOLVE = 1e-13
+
+
+@pytest.fixture(scope="module")
+def ser():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2507_00156_b200 as ser
+
+    ser._lib.load()
+    return ser
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def run_gpu(ser, block, mode=3, **kw):
+    u, v = ser.evaluate_block(block, mode=mode, **kw)
+    return (None if u is None else u.cpu().numpy()), (None if v is None else v.cpu().numpy())
+
+
+def check_block(ser, block, localized=False, mode=3, tol=TOL, **kw):
+    u, v = run_gpu(ser, block, mode=mode, **kw)
+    ur, vr = oracle.evaluate_block(block, mode=mode, localized=localized)
+    out = {}
+    if mode & 1:
+        out["u"] = rel(u, ur)
+        assert out["u"] <= tol, out
+    if mode & 2:
+        out["v"] = rel(v, vr)
+        assert out["v"] <= tol, out
+    return out
+
+
+def test_config1_full_parity(ser):
+    """Config 1 (sphere 1/h = 16, 504 targets at b/h in {0,+-1,+-2,+-3}) vs definition-mode oracle."""
+    blk = config1()
+    check_block(ser, blk, localized=False)
+    check_block(ser, blk, localized=True)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_config1_single_modes(ser, mode):
+    check_block(ser, config1(), mode=mode)
+
+
+def test_config1_closed_form_densities(ser):
+    for f, q in ((ConstField((1.0, 0.0, 0.0)), ConstField((1.0, -2.0, 0.5))),
+                 (RigidField(Omega=(0.3, -0.5, 0.7)), RigidField(U=(0.2, 0.1, -0.4), Omega=(1.0, 0.5, -0.25)))):
+        check_block(ser, config1(f_field=f, q_field=q))
+
+
+def test_per_delta_sums(ser):
+    """stokes_er_eval_deltas vs the oracle's per-delta values (localized)."""
+    blk = config1()
+    arrs = ser.to_device(blk)
+    ud, vd = ser.eval_deltas(*arrs, blk.h, blk.rho)
+    ur, vr = oracle.eval_deltas_block(blk, localized=True)
+    for k in range(3):
+        assert rel(ud[k].cpu().numpy(), ur[k]) <= TOL
+        assert rel(vd[k].cpu().numpy(), vr[k]) <= TOL
+
+
+def test_extrapolation_solve(ser):
+    """stokes_er_extrapolate (closed-form cofactor weights) vs the oracle's pivoted elimination."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    M, C, h = 4096, 6, 1 / 64
+    b = np.concatenate([np.zeros(64), rng.uniform(-4 * h, 4 * h, M - 128), rng.uniform(-30 * h, 30 * h, 64)])
+    ind = rng.standard_normal((3, C, M))
+    ref = oracle.extrapolate(b, h, (2, 3, 4), ind)
+    got = ser.extrapolate(torch.from_numpy(b).cuda(), h, (2, 3, 4), torch.from_numpy(ind).cuda()).cpu().numpy()
+    assert rel(got, ref) <= TOL_SOLVE
+
+
+def test_config2_h32_full(ser):
+    blk = config2(inv_h=32)
+    check_block(ser, blk, localized=True)
+
+
+def _sampled(ser, block, k=512, seed=1, mode=3, **kw):
+    """Full-size GPU run (the bench launch configuration), oracle on a target sample."""
+    u, v = run_gpu(ser, block, mode=mode, **kw)
+    rng = np.random.default_rng(seed)
+    idx = np.unique(np.concatenate([[0, block.M - 1], rng.choice(block.M, k, replace=False)]))
+    sub = block.take_targets(idx)
+    ur, vr = oracle.evaluate_block(sub, mode=mode, localized=False)
+    return rel(u[:, idx], ur), rel(v[:, idx], vr)
+
+
+def test_config2_h64_sampled(ser):
+    eu, ev = _sampled(ser, config2(inv_h=64))
+    assert eu <= TOL and ev <= TOL
+
+
+def test_config3_ellipsoid_sampled(ser):
+    eu, ev = _sampled(ser, config3(inv_h=64), k=384)
+    assert eu <= TOL and ev <= TOL
+
+
+def test_config4_two_spheres_sampled(ser):
+    for blk in config4(eps=0.02, inv_h=32):
+        eu, ev = _sampled(ser, blk, k=256)
+        assert eu <= TOL and ev <= TOL, blk.name
+
+
+def test_config5_h128_sampled(ser):
+    eu, ev = _sampled(ser, config5(inv_h=128), k=96)
+    assert eu <= TOL and ev <= TOL
+
+
+def test_tunings_agree(ser):
+    """targets/thread 2 vs 4 and different source chunkings: same sums up to rounding order."""
+    blk = config2(inv_h=32)
+    base = run_gpu(ser, blk)
+    for T, ch in ((4, 0), (2, 1), (4, 7)):
+        o = ser.Options()
+        o.targets_per_thread = T
+        o.source_chunk_tiles = ch
+        u, v = run_gpu(ser, blk, options=o)
+        assert rel(u, base[0]) <= 1e-13 and rel(v, base[1]) <= 1e-13
+
+
+def test_deterministic(ser):
+    blk = config2(inv_h=32)
+    a = run_gpu(ser, blk)
+    b = run_gpu(ser, blk)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_source_permutation_invariance(ser):
+    import dataclasses
+
+    blk = config2(inv_h=32)
+    perm = np.random.default_rng(2).permutation(blk.N)
+    pb = dataclasses.replace(blk, src_xyz=np.ascontiguousarray(blk.src_xyz[:, perm]),
+                             src_normal=np.ascontiguousarray(blk.src_normal[:, perm]),
+                             src_weight=np.ascontiguousarray(blk.src_weight[perm]),
+                             f=np.ascontiguousarray(blk.f[:, perm]), q=np.ascontiguousarray(blk.q[:, perm]))
+    a = run_gpu(ser, blk)
+    b = run_gpu(ser, pb)
+    assert rel(b[0], a[0]) <= 1e-13 and rel(b[1], a[1]) <= 1e-13
+
+
+def test_host_entry_point_matches_device(ser):
+    blk = config1()
+    ud, vd = run_gpu(ser, blk)
+    uh, vh = ser.evaluate_host(*blk.arrays(), blk.h, blk.rho)
+    np.testing.assert_array_equal(uh.numpy(), ud)
+    np.testing.assert_array_equal(vh.numpy(), vd)
+
+
+@pytest.mark.parametrize("m", [1, 7, 255, 256, 257, 1000])
+def test_ragged_target_counts(ser, m):
+    blk = config2(inv_h=16)
+    sub = blk.take_targets(np.arange(m) * 3 % blk.M)
+    check_block(ser, sub, localized=True)
+
+
+def test_single_source_and_tiny(ser):
+    blk = config1(inv_h=4, per_class=2)
+    check_block(ser, blk)
+    import dataclasses
+    one = dataclasses.replace(blk, src_xyz=blk.src_xyz[:, :1].copy(), src_normal=blk.src_normal[:, :1].copy(),
+                              src_weight=blk.src_weight[:1].copy(), f=blk.f[:, :1].copy(), q=blk.q[:, :1].copy())
+    check_block(ser, one)
+
+
+def test_empty_targets_and_errors(ser):
+    import torch
+
+    blk = config1(inv_h=8, per_class=1)
+    arrs = list(ser.to_device(blk))
+    e = [a[..., :0].contiguous() for a in arrs[5:]]
+    u, v = ser.evaluate(*arrs[:5], *e, blk.h, blk.rho)
+    assert u.shape == (3, 0) and v.shape == (3, 0)
+    with pytest.raises(ser.StokesERError) as ei:
+        ser.evaluate(*arrs, -1.0, blk.rho)
+    assert ei.value.status == 1
+    with pytest.raises(ser.StokesERError):
+        ser.evaluate(*arrs, blk.h, (2.0, 2.0, 4.0))
+    ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ser.StokesERError) as ei:
+        ser.evaluate(*arrs, blk.h, blk.rho, workspace=ws)
+    assert ei.value.status == 3
+
+
+def test_far_targets_pass_through(ser):
+    """|b| > 6 delta_max: no near pairs, weights (1,0,0); compare with the oracle."""
+    from workloads.configs import pure_far
+    blk = pure_far(inv_h=32, b=0.9)
+    blk = blk.take_targets(np.arange(0, blk.M, 11))
+    check_block(ser, blk, localized=False)
