@@ -230,13 +230,11 @@ def main():
     stream = torch.cuda.current_stream(dev)
     K, W = args.steps, args.warmup
 
-    def step(ev_pair=None):
-        if ev_pair is not None:
-            opt.pair_kernel_start_event = ev_pair[0].cuda_event
-            opt.pair_kernel_end_event = ev_pair[1].cuda_event
-        else:
-            opt.pair_kernel_start_event = None
-            opt.pair_kernel_end_event = None
+    def step(ev_pair=None, ev_near=None):
+        opt.pair_kernel_start_event = ev_pair[0].cuda_event if ev_pair else None
+        opt.pair_kernel_end_event = ev_pair[1].cuda_event if ev_pair else None
+        opt.near_kernel_start_event = ev_near[0].cuda_event if ev_near else None
+        opt.near_kernel_end_event = ev_near[1].cuda_event if ev_near else None
         ser.evaluate(*arrs, block.h, block.rho, out_u=out_u, out_v=out_v, workspace=ws, stream=stream,
                      options=opt)
 
@@ -247,7 +245,8 @@ def main():
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     evp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    for a, b in evp:  # torch creates the CUDA event lazily on first record: materialize the handles
+    evn = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for a, b in evp + evn:  # torch creates the CUDA event lazily on first record: materialize the handles
         a.record(stream)
         b.record(stream)
     if dist is not None:
@@ -257,7 +256,7 @@ def main():
         for i in range(K):
             flush.zero_()  # L2 flush, outside the timed events
             ev[i][0].record(stream)
-            step(evp[i])
+            step(evp[i], evn[i])
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
     if dist is not None:
@@ -265,6 +264,7 @@ def main():
     torch.cuda.synchronize(dev)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     pair_ms = [a.elapsed_time(b) for a, b in evp]
+    near_ms = [a.elapsed_time(b) for a, b in evn]
     total_s = sum(step_ms) / 1e3
     if dist is not None:
         t = torch.tensor([total_s], dtype=torch.float64, device=dev)
@@ -309,22 +309,29 @@ def main():
         return
 
     clocks = clk.summary()
-    pair_avg_s = statistics.mean(pair_ms) / 1e3
+    far_avg_s = statistics.mean(pair_ms) / 1e3
+    near_avg_s = statistics.mean(near_ms) / 1e3
     far = pairs - near
-    alg_flops = far * F_FAR_ALG + near * F_NEAR_ALG
     f_clk = 1965.0
     peak = SMS * FP64_LANES_PER_SM * 2 * f_clk * 1e6 / 1e12  # TFLOP/s
-    achieved = alg_flops / pair_avg_s / 1e12
+    far_flops = far * F_FAR_ALG
+    achieved = far_flops / far_avg_s / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": None,
-                "kernel": "pair_kernel<3,2> (FP64 pipe)",
+                "kernel": "far_kernel<3,T> (FP64 pipe): the shared far-field sum, PAPER.md:183-191",
                 "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM (DFMA-loop probe) x 2 x 1965 MHz max SM clock",
-                "flops_per_launch": alg_flops, "flop_convention": f"far {F_FAR_ALG}, near {F_NEAR_ALG} algorithmic",
-                "far_issued_frac": (far * F_FAR_ISSUED + near * F_NEAR_ALG) / pair_avg_s / 1e12 / peak,
-                "pair_kernel_ms": pair_avg_s * 1e3,
-                "pair_kernel_share": sum(pair_ms) / sum(step_ms)}
+                "flops_per_launch": far_flops, "flop_convention": f"{F_FAR_ALG} algorithmic flops per far pair "
+                                                                   "(rsqrt = 1, FMA = 2)",
+                "frac_issued_convention": far * F_FAR_ISSUED / far_avg_s / 1e12 / peak,
+                "far_kernel_ms": far_avg_s * 1e3,
+                "far_kernel_share": sum(pair_ms) / sum(step_ms),
+                "far_pairs_per_s": far / far_avg_s}
     if clocks.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (SMS * FP64_LANES_PER_SM * 2 * clocks["sm_mhz"] / 1e6)
+    near_info = {"kernel": "near_kernel<3>", "ms": near_avg_s * 1e3, "share": sum(near_ms) / sum(step_ms),
+                 "near_pairs": near, "near_pairs_per_s": near / near_avg_s,
+                 "tflops_alg": near * F_NEAR_ALG / near_avg_s / 1e12}
+    alg_flops = far * F_FAR_ALG + near * F_NEAR_ALG
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
@@ -335,9 +342,9 @@ def main():
                        "grid_ctas": int(opt.stats[1]), "chunk_tiles": int(opt.stats[2]),
                        "parallelism": f"target-sharded x{world} (independent instances)"},
             "fp64_tflops_alg": alg_flops * K * world / total_s / 1e12,
-            "roofline": roofline, "clocks": clocks,
+            "roofline": roofline, "near_kernel": near_info, "clocks": clocks,
             "gpu_launches": K * ser.launch_count(M, N, 3),
-            "gpu_launches_note": "our kernels per step: bbox, 2 morton, pack_sources, pack_targets, pair, finalize "
+            "gpu_launches_note": "our kernels per step: bbox, 2 morton, pack_sources, pack_targets, far, near, finalize "
                                  "(+ CUB radix-sort launches, library code)",
             "e2e": e2e}
     if not args.no_cpu_baseline and world == 1:

@@ -138,14 +138,16 @@ int stokes_er_extrapolate(const double* tgt_b, int64_t M, double h, const double
 int stokes_er_launch_count(int64_t M, int64_t N, int mode);
 
 /* Optional profiling hooks for bench.py: if non-NULL, cudaEvent_t handles
- * (as void*) recorded on `stream` immediately before / after the pair-sum
- * kernel (the dominant kernel) of the NEXT stokes_er_eval_ex call. */
+ * (as void*) recorded on `stream` immediately before / after the far-field
+ * pair-sum kernel (the dominant kernel) of this stokes_er_eval_ex call. */
 typedef struct {
   void* pair_kernel_start_event;
   void* pair_kernel_end_event;
   int targets_per_thread; /* 0 = default; 2 or 4 (tuning/tests)          */
   int source_chunk_tiles; /* 0 = automatic; work item = chunk * 128 sources */
   int64_t stats[4];       /* out: [0] work items, [1] grid CTAs, [2] chunk tiles, [3] targets/thread */
+  void* near_kernel_start_event; /* optional events around the near-field kernel */
+  void* near_kernel_end_event;
 } stokes_er_options;
 
 /* Workspace for stokes_er_eval_ex with these tuning options (>= stokes_er_workspace_bytes

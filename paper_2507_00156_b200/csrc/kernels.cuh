@@ -58,6 +58,16 @@ struct PairParams {
   double inv_delta[3];
 };
 
+struct NearParams {
+  const double* src;      // [Npad][12]
+  const double* src_box;  // [Npad/32][8]
+  const double* tgt;      // [14][Mpad]
+  double* near_out;       // [6][Mpad]
+  int64_t Mpad, Npad;
+  double rc2, rc2_box, r2_tiny;
+  double inv_delta[3];
+};
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -284,80 +294,39 @@ __device__ __forceinline__ void far_pair(const Src& s, const Tgt& t, Acc& a) {
   }
 }
 
-// Near pair (r <= c delta_max): the three regularized kernels folded with the
-// extrapolation weights w_k (DESIGN.md Sec. 5.2):
-//   S_i = sum_k w_k s_i(r/delta_k),  C = sum_k w_k (s2 - s3)(r/delta_k)
-//   u += g S1/r + d (d.g) S2/r^3                                  (eq. 12)
-//   v += d (d.dq)(d.mw) S3/r^5 + P C/r^3,  P = t1 contracted      (eq. 13 with
-//        eq. 7 rearranged: T1 s2 + T2 s3 = -6[yyy s3/r^5 + t1 (s2-s3)/r^3])
+// Far pair with the near pairs of a mixed sub-tile masked out: ri := 0 zeroes
+// every term of far_pair (u += (g + d a3) 0, c = .. ri^5 = 0) at the cost of
+// one compare and a select; the near kernel owns those pairs.
 template <int MODE>
-__device__ __forceinline__ Acc near_pair(const Src& s, const Tgt& t, const PairParams& p, int64_t ti) {
-  Acc a{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+__device__ __forceinline__ void far_pair_masked(const Src& s, const Tgt& t, Acc& a, double rc2) {
   const double dx = t.y0 - s.x, dy = t.y1 - s.y, dz = t.y2 - s.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-  const double* tg = p.tgt + ti;
-  const int64_t Mp = p.Mpad;
-  const double w0 = __ldg(tg + F_W0 * Mp), w1 = __ldg(tg + F_W1 * Mp), w2 = __ldg(tg + F_W2 * Mp);
-  double A1, A3, A5, AP;
-  if (r2 < p.r2_tiny) {  // r -> 0 limits (DESIGN.md R3)
-    const double i0 = p.inv_delta[0], i1 = p.inv_delta[1], i2 = p.inv_delta[2];
-    A1 = kTwoOverSqrtPi * (w0 * i0 + w1 * i1 + w2 * i2);
-    A3 = (2.0 / 3.0) * kTwoOverSqrtPi * (w0 * i0 * i0 * i0 + w1 * i1 * i1 * i1 + w2 * i2 * i2 * i2);
-    A5 = (4.0 / 15.0) * kTwoOverSqrtPi *
-         (w0 * i0 * i0 * i0 * i0 * i0 + w1 * i1 * i1 * i1 * i1 * i1 + w2 * i2 * i2 * i2 * i2 * i2);
-    AP = A3;
-  } else {
-    const double ri = rsqrt_nr(r2);
-    const double r = r2 * ri;
-    double S1 = 0.0, S2 = 0.0, S3 = 0.0, C = 0.0;
-    const double wk[3] = {w0, w1, w2};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      double s1, s2, s3, c23;
-      s_factors(r * p.inv_delta[k], s1, s2, s3, c23);
-      S1 = fma(wk[k], s1, S1);
-      S2 = fma(wk[k], s2, S2);
-      S3 = fma(wk[k], s3, S3);
-      C = fma(wk[k], c23, C);
-    }
-    const double ri3 = ri * ri * ri;
-    A1 = S1 * ri;
-    A3 = S2 * ri3;
-    A5 = S3 * ri3 * ri * ri;
-    AP = C * ri3;
-  }
+  const double ri = r2 > rc2 ? rsqrt_nr(r2) : 0.0;
+  const double ri2 = ri * ri;
   if (MODE & 1) {
     const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
-    const double dg = fma(dx, gx, fma(dy, gy, dz * gz)) * A3;
-    a.u0 = fma(gx, A1, dx * dg);
-    a.u1 = fma(gy, A1, dy * dg);
-    a.u2 = fma(gz, A1, dz * dg);
+    const double a3 = fma(dx, gx, fma(dy, gy, dz * gz)) * ri2;
+    a.u0 = fma(fma(dx, a3, gx), ri, a.u0);
+    a.u1 = fma(fma(dy, a3, gy), ri, a.u1);
+    a.u2 = fma(fma(dz, a3, gz), ri, a.u2);
   }
   if (MODE & 2) {
-    const double n0 = __ldg(tg + F_N0 * Mp), n1 = __ldg(tg + F_N1 * Mp), n2 = __ldg(tg + F_N2 * Mp);
-    const double b = __ldg(tg + F_B * Mp);
     const double qx = s.qx - t.q0, qy = s.qy - t.q1, qz = s.qz - t.q2;
     const double dq = fma(dx, qx, fma(dy, qy, dz * qz));
     const double dm = fma(dx, s.mx, fma(dy, s.my, dz * s.mz));
-    const double c = dq * dm * A5;
-    // xh = x - x0 = b n0 - (y - x)   (y = x0 + b n0, PAPER.md:107)
-    const double hx = fma(b, n0, -dx), hy = fma(b, n1, -dy), hz = fma(b, n2, -dz);
-    const double an = fma(n0, qx, fma(n1, qy, n2 * qz));          // n0.dq
-    const double cn = fma(n0, s.mx, fma(n1, s.my, n2 * s.mz));    // n0.mw
-    const double dd = fma(hx, qx, fma(hy, qy, hz * qz));          // xh.dq
-    const double e = fma(hx, s.mx, fma(hy, s.my, hz * s.mz));     // xh.mw
-    const double ac = an * cn;
-    const double pn = (fma(b, ac, -dd * cn) - an * e) * AP;       // n0 coefficient of t1 contraction
-    const double ph = ac * AP;                                    // xh coefficient (with minus)
-    a.v0 = fma(dx, c, fma(n0, pn, -hx * ph));
-    a.v1 = fma(dy, c, fma(n1, pn, -hy * ph));
-    a.v2 = fma(dz, c, fma(n2, pn, -hz * ph));
+    const double c = (dq * dm) * (ri2 * ri2 * ri);
+    a.v0 = fma(dx, c, a.v0);
+    a.v1 = fma(dy, c, a.v1);
+    a.v2 = fma(dz, c, a.v2);
   }
-  return a;
 }
 
+// K1: far-field pair sums (the non-local part, computed once
+// and shared by the three deltas).  Persistent CTAs pull (target block,
+// source chunk) items from a queue; each item's partial sums go to their own
+// slot, summed in fixed order by the finalize (deterministic).
 template <int MODE, int T>
-__global__ void __launch_bounds__(kThreads) pair_kernel(const PairParams p) {
+__global__ void __launch_bounds__(kThreads) far_kernel(const PairParams p) {
   __shared__ __align__(128) double tile[2][kTile * kSrcDoubles];
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int s_item;
@@ -388,12 +357,10 @@ __global__ void __launch_bounds__(kThreads) pair_kernel(const PairParams p) {
     // targets of this thread: warp-contiguous (Morton order) -> tight warp boxes
     Tgt tg[T];
     Acc acc[T];
-    int64_t tix[T];
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
 #pragma unroll
     for (int j = 0; j < T; ++j) {
       const int64_t i = (int64_t)tb * TB + warp * 32 * T + j * 32 + lane;
-      tix[j] = i;
       const double* q = p.tgt + i;
       tg[j].y0 = q[F_Y0 * p.Mpad];
       tg[j].y1 = q[F_Y1 * p.Mpad];
@@ -441,35 +408,12 @@ __global__ void __launch_bounds__(kThreads) pair_kernel(const PairParams p) {
 #pragma unroll
             for (int j = 0; j < T; ++j) far_pair<MODE>(s, tg[j], acc[j]);
           }
-        } else {
-#pragma unroll 1
+        } else {  // mixed: far pairs only, near pairs belong to the near kernel
+#pragma unroll 2
           for (int k = 0; k < kSub; ++k) {
             const Src s = load_src<MODE>(ss + k * kSrcDoubles);
-            unsigned near_mask = 0;
 #pragma unroll
-            for (int j = 0; j < T; ++j) {
-              const double dx = tg[j].y0 - s.x, dy = tg[j].y1 - s.y, dz = tg[j].y2 - s.z;
-              const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-              if (r2 > p.rc2) far_pair<MODE>(s, tg[j], acc[j]);
-              else near_mask |= 1u << j;
-            }
-            // one (non-unrolled) copy of the near code serves all T targets
-            while (near_mask) {
-              const int j = __ffs(near_mask) - 1;
-              near_mask &= near_mask - 1;
-              Tgt t = tg[0];
-              int64_t ti = tix[0];
-#pragma unroll
-              for (int jj = 1; jj < T; ++jj)
-                if (jj == j) { t = tg[jj]; ti = tix[jj]; }
-              const Acc d = near_pair<MODE>(s, t, p, ti);
-#pragma unroll
-              for (int jj = 0; jj < T; ++jj)
-                if (jj == j) {
-                  acc[jj].u0 += d.u0; acc[jj].u1 += d.u1; acc[jj].u2 += d.u2;
-                  acc[jj].v0 += d.v0; acc[jj].v1 += d.v1; acc[jj].v2 += d.v2;
-                }
-            }
+            for (int j = 0; j < T; ++j) far_pair_masked<MODE>(s, tg[j], acc[j], p.rc2);
           }
         }
       }
@@ -487,11 +431,215 @@ __global__ void __launch_bounds__(kThreads) pair_kernel(const PairParams p) {
   }
 }
 
+// ------------------------------------------------------------ K3: near pairs
+// Target record in SMEM for the near kernel (16 doubles).
+struct NearTgt {
+  double y0, y1, y2, alpha, q0, q1, q2, n0, n1, n2, b, w0, w1, w2, pad0, pad1;
+};
+
+// Near pair (r <= c delta_max): the three regularized kernels folded with the
+// extrapolation weights w_k (DESIGN.md Sec. 5.2):
+//   S_i = sum_k w_k s_i(r/delta_k),  C = sum_k w_k (s2 - s3)(r/delta_k)
+//   u = g S1/r + d (d.g) S2/r^3                                   (eq. 12)
+//   v = d (d.dq)(d.mw) S3/r^5 + P C/r^3,  P = t1 contracted        (eq. 13 with
+//       eq. 7 rearranged: T1 s2 + T2 s3 = -6[yyy s3/r^5 + t1 (s2-s3)/r^3])
+template <int MODE>
+__device__ __forceinline__ Acc near_pair(const Src& s, const NearTgt& t, const NearParams& p) {
+  Acc a{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const double dx = t.y0 - s.x, dy = t.y1 - s.y, dz = t.y2 - s.z;
+  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+  double A1, A3, A5, AP;
+  if (r2 < p.r2_tiny) {  // r -> 0 limits (DESIGN.md R3)
+    const double i0 = p.inv_delta[0], i1 = p.inv_delta[1], i2 = p.inv_delta[2];
+    A1 = kTwoOverSqrtPi * (t.w0 * i0 + t.w1 * i1 + t.w2 * i2);
+    A3 = (2.0 / 3.0) * kTwoOverSqrtPi * (t.w0 * i0 * i0 * i0 + t.w1 * i1 * i1 * i1 + t.w2 * i2 * i2 * i2);
+    A5 = (4.0 / 15.0) * kTwoOverSqrtPi *
+         (t.w0 * i0 * i0 * i0 * i0 * i0 + t.w1 * i1 * i1 * i1 * i1 * i1 + t.w2 * i2 * i2 * i2 * i2 * i2);
+    AP = A3;
+  } else {
+    const double ri = rsqrt_nr(r2);
+    const double r = r2 * ri;
+    double S1 = 0.0, S2 = 0.0, S3 = 0.0, C = 0.0;
+    const double wk[3] = {t.w0, t.w1, t.w2};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double s1, s2, s3, c23;
+      s_factors(r * p.inv_delta[k], s1, s2, s3, c23);
+      S1 = fma(wk[k], s1, S1);
+      S2 = fma(wk[k], s2, S2);
+      S3 = fma(wk[k], s3, S3);
+      C = fma(wk[k], c23, C);
+    }
+    const double ri3 = ri * ri * ri;
+    A1 = S1 * ri;
+    A3 = S2 * ri3;
+    A5 = S3 * ri3 * ri * ri;
+    AP = C * ri3;
+  }
+  if (MODE & 1) {
+    const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
+    const double dg = fma(dx, gx, fma(dy, gy, dz * gz)) * A3;
+    a.u0 = fma(gx, A1, dx * dg);
+    a.u1 = fma(gy, A1, dy * dg);
+    a.u2 = fma(gz, A1, dz * dg);
+  }
+  if (MODE & 2) {
+    const double n0 = t.n0, n1 = t.n1, n2 = t.n2, b = t.b;
+    const double qx = s.qx - t.q0, qy = s.qy - t.q1, qz = s.qz - t.q2;
+    const double dq = fma(dx, qx, fma(dy, qy, dz * qz));
+    const double dm = fma(dx, s.mx, fma(dy, s.my, dz * s.mz));
+    const double c = dq * dm * A5;
+    // xh = x - x0 = b n0 - (y - x)   (y = x0 + b n0, PAPER.md:107)
+    const double hx = fma(b, n0, -dx), hy = fma(b, n1, -dy), hz = fma(b, n2, -dz);
+    const double an = fma(n0, qx, fma(n1, qy, n2 * qz));          // n0.dq
+    const double cn = fma(n0, s.mx, fma(n1, s.my, n2 * s.mz));    // n0.mw
+    const double dd = fma(hx, qx, fma(hy, qy, hz * qz));          // xh.dq
+    const double e = fma(hx, s.mx, fma(hy, s.my, hz * s.mz));     // xh.mw
+    const double ac = an * cn;
+    const double pn = (fma(b, ac, -dd * cn) - an * e) * AP;       // n0 coefficient of t1 contraction
+    const double ph = ac * AP;                                    // xh coefficient (with minus)
+    a.v0 = fma(dx, c, fma(n0, pn, -hx * ph));
+    a.v1 = fma(dy, c, fma(n1, pn, -hy * ph));
+    a.v2 = fma(dz, c, fma(n2, pn, -hz * ph));
+  }
+  return a;
+}
+
+// K3: near-field pairs.  One warp owns 32 Morton-consecutive targets (lane l
+// accumulates target l).  It finds the 32-source sub-tiles whose box is
+// within c delta_max of its target box, tests the 32 x 32 candidate pairs,
+// compacts the near ones into a target-major list (ballot transpose + warp
+// prefix sum) and evaluates the list 32 pairs at a time with all lanes busy.
+// Each target's results are added in list order: deterministic.
+constexpr int kNearWarps = 4;
+template <int MODE>
+__global__ void __launch_bounds__(kNearWarps * 32) near_kernel(const NearParams p) {
+  __shared__ __align__(16) NearTgt s_tgt[kNearWarps][32];
+  __shared__ __align__(16) double s_src[kNearWarps][32 * kSrcDoubles];
+  __shared__ __align__(16) double s_res[kNearWarps][32][6];
+  __shared__ uint16_t s_list[kNearWarps][32 * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * kNearWarps + warp;  // target group
+  if (g * 32 >= p.Mpad) return;
+  const int64_t ti = g * 32 + lane;
+  {
+    NearTgt t;
+    const double* q = p.tgt + ti;
+    t.y0 = q[F_Y0 * p.Mpad]; t.y1 = q[F_Y1 * p.Mpad]; t.y2 = q[F_Y2 * p.Mpad];
+    t.alpha = q[F_ALPHA * p.Mpad];
+    t.q0 = q[F_Q0 * p.Mpad]; t.q1 = q[F_Q1 * p.Mpad]; t.q2 = q[F_Q2 * p.Mpad];
+    t.n0 = q[F_N0 * p.Mpad]; t.n1 = q[F_N1 * p.Mpad]; t.n2 = q[F_N2 * p.Mpad];
+    t.b = q[F_B * p.Mpad];
+    t.w0 = q[F_W0 * p.Mpad]; t.w1 = q[F_W1 * p.Mpad]; t.w2 = q[F_W2 * p.Mpad];
+    t.pad0 = t.pad1 = 0.0;
+    s_tgt[warp][lane] = t;
+  }
+  double lo[3], hi[3];
+  lo[0] = hi[0] = s_tgt[warp][lane].y0;
+  lo[1] = hi[1] = s_tgt[warp][lane].y1;
+  lo[2] = hi[2] = s_tgt[warp][lane].y2;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    for (int o = 16; o; o >>= 1) {
+      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+  __syncwarp();
+  Acc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int n_sub = static_cast<int>(p.Npad / kSub);
+  for (int base = 0; base < n_sub; base += 32) {
+    bool mixed = false;
+    const int sb = base + lane;
+    if (sb < n_sub) {
+      const double* bx = p.src_box + (int64_t)sb * 8;
+      double g2 = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double gap = fmax(0.0, fmax(bx[d] - hi[d], lo[d] - bx[4 + d]));
+        g2 = fma(gap, gap, g2);
+      }
+      mixed = g2 <= p.rc2_box;
+    }
+    unsigned mm = __ballot_sync(0xffffffffu, mixed);
+    while (mm) {
+      const int sub = base + __ffs(mm) - 1;
+      mm &= mm - 1;
+      // stage the 32 sources of this sub-tile (lane l loads source l)
+      {
+        const double2* gs = reinterpret_cast<const double2*>(p.src + ((int64_t)sub * kSub + lane) * kSrcDoubles);
+        double2* ds = reinterpret_cast<double2*>(&s_src[warp][lane * kSrcDoubles]);
+#pragma unroll
+        for (int k = 0; k < kSrcDoubles / 2; ++k) ds[k] = gs[k];
+      }
+      __syncwarp();
+      // lane l (as source l): which targets are near?
+      const double sx = s_src[warp][lane * kSrcDoubles + 0], sy = s_src[warp][lane * kSrcDoubles + 1],
+                   sz = s_src[warp][lane * kSrcDoubles + 2];
+      unsigned tmask = 0;
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const double dx = s_tgt[warp][t].y0 - sx, dy = s_tgt[warp][t].y1 - sy, dz = s_tgt[warp][t].y2 - sz;
+        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+        tmask |= (r2 <= p.rc2 ? 1u : 0u) << t;
+      }
+      // transpose: lane t gets the mask of its near sources
+      unsigned smask = 0;
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const unsigned b = __ballot_sync(0xffffffffu, (tmask >> t) & 1u);
+        if (lane == t) smask = b;
+      }
+      const int cnt = __popc(smask);
+      int pre = cnt;  // inclusive warp scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, pre, 31);
+      const int start = pre - cnt;
+      {  // target-major pair list: (target << 5) | source
+        unsigned m = smask;
+        int pos = start;
+        while (m) {
+          const int sidx = __ffs(m) - 1;
+          m &= m - 1;
+          s_list[warp][pos++] = static_cast<uint16_t>((lane << 5) | sidx);
+        }
+      }
+      __syncwarp();
+      for (int rb = 0; rb < total; rb += 32) {
+        const int pidx = rb + lane;
+        if (pidx < total) {
+          const int code = s_list[warp][pidx];
+          const Src s = load_src<MODE>(&s_src[warp][(code & 31) * kSrcDoubles]);
+          const Acc d = near_pair<MODE>(s, s_tgt[warp][code >> 5], p);
+          s_res[warp][lane][0] = d.u0; s_res[warp][lane][1] = d.u1; s_res[warp][lane][2] = d.u2;
+          s_res[warp][lane][3] = d.v0; s_res[warp][lane][4] = d.v1; s_res[warp][lane][5] = d.v2;
+        }
+        __syncwarp();
+        // lane t adds its own entries of this round, in list order
+        const int lo_i = max(start, rb), hi_i = min(start + cnt, rb + 32);
+        for (int k = lo_i; k < hi_i; ++k) {
+          const double* r = s_res[warp][k - rb];
+          acc.u0 += r[0]; acc.u1 += r[1]; acc.u2 += r[2];
+          acc.v0 += r[3]; acc.v1 += r[4]; acc.v2 += r[5];
+        }
+        __syncwarp();
+      }
+    }
+  }
+  double* out = p.near_out + ti;
+  out[0 * p.Mpad] = acc.u0; out[1 * p.Mpad] = acc.u1; out[2 * p.Mpad] = acc.u2;
+  out[3 * p.Mpad] = acc.v0; out[4 * p.Mpad] = acc.v1; out[5 * p.Mpad] = acc.v2;
+}
+
 // ------------------------------------------------------------ K2: finalize
 template <int MODE>
-__global__ void finalize_kernel(const double* __restrict__ partial, const double* __restrict__ tgt,
-                                const int32_t* __restrict__ orig, int64_t M, int64_t Mpad, int n_chunks, int TB,
-                                double* __restrict__ out_u, double* __restrict__ out_v) {
+__global__ void finalize_kernel(const double* __restrict__ partial, const double* __restrict__ near_out,
+                                const double* __restrict__ tgt, const int32_t* __restrict__ orig, int64_t M,
+                                int64_t Mpad, int n_chunks, int TB, double* __restrict__ out_u,
+                                double* __restrict__ out_v) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= M) return;
   const int64_t tb = i / TB, loc = i - tb * TB;
@@ -502,6 +650,9 @@ __global__ void finalize_kernel(const double* __restrict__ partial, const double
     for (int c = 0; c < 6; ++c)
       if ((c < 3 && (MODE & 1)) || (c >= 3 && (MODE & 2))) s[c] += pp[c * TB];
   }
+#pragma unroll
+  for (int c = 0; c < 6; ++c)
+    if ((c < 3 && (MODE & 1)) || (c >= 3 && (MODE & 2))) s[c] += near_out[c * Mpad + i];
   const int64_t o = orig[i];
   const double inv8pi = 1.0 / (8.0 * kPi);
   if (MODE & 1)

@@ -126,7 +126,7 @@ struct Plan {
   int n_tiles = 0, n_tblocks = 0, chunk_tiles = 0, n_chunks = 0, n_items = 0;
   size_t cub_bytes = 0;
   size_t off_box, off_skin, off_skout, off_svin, off_svout, off_tkin, off_tkout, off_tvin, off_tvout;
-  size_t off_cub, off_src, off_srcbox, off_tgt, off_orig, off_partial, off_counter, total;
+  size_t off_cub, off_src, off_srcbox, off_tgt, off_orig, off_partial, off_near, off_counter, total;
 };
 
 size_t cub_sort_bytes(int64_t n) {
@@ -180,6 +180,7 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override) {
   p.off_tgt = take(p.Mpad * kTgtFields * sizeof(double));
   p.off_orig = take(p.Mpad * sizeof(int32_t));
   p.off_partial = take((size_t)p.n_items * 6 * TB * sizeof(double));
+  p.off_near = take((size_t)p.Mpad * 6 * sizeof(double));
   p.off_counter = take(sizeof(int) * 4);
   p.total = off;
   return p;
@@ -216,10 +217,10 @@ void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_kernel<MODE, T>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, far_kernel<MODE, T>, kThreads, 0);
   const int grid = std::max(1, std::min(pp.n_items, sms * std::max(occ, 1)));
   *grid_out = grid;
-  pair_kernel<MODE, T><<<grid, kThreads, 0, s>>>(pp);
+  far_kernel<MODE, T><<<grid, kThreads, 0, s>>>(pp);
 }
 
 template <int MODE>
@@ -241,6 +242,7 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   double* tgt = reinterpret_cast<double*>(ws + P.off_tgt);
   int32_t* orig = reinterpret_cast<int32_t*>(ws + P.off_orig);
   double* partial = reinterpret_cast<double*>(ws + P.off_partial);
+  double* near_out = reinterpret_cast<double*>(ws + P.off_near);
   int* counter = reinterpret_cast<int*>(ws + P.off_counter);
 
   bbox_kernel<<<1, 1024, 0, s>>>(sx, N, ty, M, box);
@@ -282,13 +284,29 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   if (P.T == 4) launch_pairs<MODE, 4>(pp, s, &grid);
   else launch_pairs<MODE, 2>(pp, s, &grid);
   if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
+
+  NearParams np;
+  np.src = src;
+  np.src_box = srcbox;
+  np.tgt = tgt;
+  np.near_out = near_out;
+  np.Mpad = P.Mpad;
+  np.Npad = P.Npad;
+  np.rc2 = pp.rc2;
+  np.rc2_box = pp.rc2_box;
+  np.r2_tiny = pp.r2_tiny;
+  for (int k = 0; k < 3; ++k) np.inv_delta[k] = pp.inv_delta[k];
+  if (opt && opt->near_kernel_start_event)
+    cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_start_event), s);
+  near_kernel<MODE><<<ceil_div(P.Mpad / 32, kNearWarps), kNearWarps * 32, 0, s>>>(np);
+  if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
   if (opt) {
     opt->stats[0] = P.n_items;
     opt->stats[1] = grid;
     opt->stats[2] = P.chunk_tiles;
     opt->stats[3] = P.T;
   }
-  finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, tgt, orig, M, P.Mpad, P.n_chunks,
+  finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad, P.n_chunks,
                                                           kThreads * P.T, out_u, out_v);
   return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
 }
@@ -441,9 +459,9 @@ int stokes_er_extrapolate(const double* tgt_b, int64_t M, double h, const double
 int stokes_er_launch_count(int64_t M, int64_t N, int mode) {
   (void)N;
   (void)mode;
-  // bbox, 2x morton, pack sources, pack targets, pair, finalize: our kernels.
+  // bbox, 2x morton, pack sources, pack targets, far, near, finalize: our kernels.
   // The two CUB radix sorts add their own launches (library code).
-  return M > 0 ? 7 : 0;
+  return M > 0 ? 8 : 0;
 }
 
 const char* stokes_er_status_string(int status) {
