@@ -9,7 +9,7 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libstokes_er.so")
+LIB_PATH = os.environ.get("STOKES_ER_LIB") or os.path.join(PKG, "libstokes_er.so")
 
 STATUS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "EWORKSPACE", 4: "EARCH"}
 

@@ -5,6 +5,8 @@
 #pragma once
 #include <cstdint>
 
+#include "sfactor_coeffs.inc"
+
 namespace ser {
 
 constexpr double kPi = 3.14159265358979323846;
@@ -82,6 +84,65 @@ __device__ __forceinline__ void s_sharp_factors(double t, double& s1, double& s2
   s2 = E - (2.0 / 3.0) * (3.0 * t - 14.0 * t3 + 4.0 * t5) * e;
   s3 = E - (2.0 / 9.0) * (9.0 * t + 6.0 * t3 - 4.0 * t5) * e;
   c23 = s2 - s3;
+}
+
+// e^{-u} for 0 <= u <= 700 (near pairs: u <= 144): Cody-Waite reduction
+// u = n ln2 + r, |r| <= ln2/2, degree-11 polynomial (tools/gen_sfactor_coeffs.py),
+// scale 2^n by building the exponent bits.  No special-case branches.
+__device__ __forceinline__ double exp_neg(double u) {
+  const double x = -u;
+  const double kd = fma(x, 1.4426950408889634074, 6755399441055744.0);  // round(x/ln2) + 1.5*2^52
+  const int n = __double2loint(kd);
+  const double nd = kd - 6755399441055744.0;
+  double r = fma(nd, -6.93147180559945286227e-01, x);
+  r = fma(nd, -2.31904681384629955842e-17, r);
+  double p = kExpPoly[kExpDeg];
+#pragma unroll
+  for (int j = kExpDeg - 1; j >= 0; --j) p = fma(p, r, kExpPoly[j]);
+  return p * __hiloint2double((n + 1023) << 20, 0);
+}
+
+// Smoothing factors at t = r/delta for t >= 0.5:
+//   E = erf t = 1 - e^{-t^2} erfcx(t), erfcx from a 6-piece degree-12 table in
+//   SMEM (rows 17 doubles apart: the pieces hit distinct banks);
+//   s2 = E - (2/sqrt pi) t e^{-t^2},  c23 = s2 - s3 = (2/sqrt pi)(2/3) t^3 e^{-t^2}.
+// Branch-free; for t < 0.5 it returns finite values the caller discards.
+__device__ __forceinline__ void sfactor_table(double t, const double* __restrict__ tab, double& E, double& s2,
+                                              double& c23) {
+  const double u = t * t;
+  const double e = exp_neg(u);
+  const double tc = fmin(t, 6.0);  // erfc(t > 6) < 2e-17: E rounds to 1 either way
+  const int hi = __double2hiint(tc);
+  const int pc = (hi >= kErfcxEdgeHi[0]) + (hi >= kErfcxEdgeHi[1]) + (hi >= kErfcxEdgeHi[2]) +
+                 (hi >= kErfcxEdgeHi[3]) + (hi >= kErfcxEdgeHi[4]);
+  const double* row = tab + pc * kErfcxStride;
+  const double x = fma(row[0], tc, row[1]);
+  double p = row[2 + kErfcxDeg];
+#pragma unroll
+  for (int j = kErfcxDeg - 1; j >= 0; --j) p = fma(p, x, row[2 + j]);
+  E = fma(-e, p, 1.0);
+  const double gt = (kTwoOverSqrtPi * e) * t;
+  s2 = E - gt;
+  c23 = gt * (2.0 / 3.0) * u;
+}
+
+// t < 0.5: s1/t, s2/t^3, s3/t^5 and (s2 - s3)/t^3 from their series in u = t^2
+// (cancellation-free, exact r -> 0 limits), scaled to A += w s_i/(t delta)^p.
+__device__ __forceinline__ void sfactor_series_add(double t, double invd, double w, double& A1, double& A3,
+                                                   double& A5, double& AP) {
+  const double u = t * t;
+  double f1 = kPhi1[kSeriesTerms - 1], f3 = kPhi3[kSeriesTerms - 1], f5 = kPhi5[kSeriesTerms - 1];
+#pragma unroll
+  for (int j = kSeriesTerms - 2; j >= 0; --j) {
+    f1 = fma(f1, u, kPhi1[j]);
+    f3 = fma(f3, u, kPhi3[j]);
+    f5 = fma(f5, u, kPhi5[j]);
+  }
+  const double wi = w * invd, wi3 = wi * invd * invd, wi5 = wi3 * invd * invd;
+  A1 = fma(wi, f1, A1);
+  A3 = fma(wi3, f3, A3);
+  A5 = fma(wi5, f5, A5);
+  AP = fma(wi3, (2.0 / 3.0) * kTwoOverSqrtPi * exp_neg(u), AP);  // (4/(3 sqrt pi)) e^{-t^2}
 }
 
 }  // namespace ser

@@ -34,7 +34,10 @@
 namespace ser {
 
 constexpr int kThreads = 128;        // threads per pair-kernel CTA (4 warps)
-constexpr int kTile = 128;           // sources per SMEM tile
+#ifndef SER_TILE
+#define SER_TILE 128
+#endif
+constexpr int kTile = SER_TILE;      // sources per SMEM tile (tuning macro)
 constexpr int kSub = 32;             // sources per classification sub-tile
 constexpr int kSrcDoubles = 12;      // packed source record: x(3) mw(3) fw(3) q(3)
 constexpr int kTgtFields = 14;       // y(3) alpha q0(3) n0(3) b w(3)
@@ -62,8 +65,10 @@ struct NearParams {
   const double* src;      // [Npad][12]
   const double* src_box;  // [Npad/32][8]
   const double* tgt;      // [14][Mpad]
-  double* near_out;       // [6][Mpad]
+  double* near_out;       // [phases][6][Mpad] partial near sums
+  int* counter;           // warp work-queue head
   int64_t Mpad, Npad;
+  int n_units, phases;    // unit = (32-target group, phase); phase p takes every phases-th mixed sub-tile
   double rc2, rc2_box, r2_tiny;
   double inv_delta[3];
 };
@@ -439,53 +444,52 @@ struct NearTgt {
 
 // Near pair (r <= c delta_max): the three regularized kernels folded with the
 // extrapolation weights w_k:
-//   S_i = sum_k w_k s_i(r/delta_k),  C = sum_k w_k (s2 - s3)(r/delta_k)
-//   u = g S1/r + d (d.g) S2/r^3                                   (eq. 12)
-//   v = d (d.dq)(d.mw) S3/r^5 + P C/r^3,  P = t1 contracted        (eq. 13 with
+//   A1 = sum_k w_k s1(r/d_k)/r, A3 = sum_k w_k s2/r^3, A5 = sum_k w_k s3/r^5,
+//   AP = sum_k w_k (s2 - s3)/r^3
+//   u = g A1 + d (d.g) A3                                         (eq. 12)
+//   v = d (d.dq)(d.mw) A5 + P AP,  P = t1 contracted               (eq. 13 with
 //       eq. 7 rearranged: T1 s2 + T2 s3 = -6[yyy s3/r^5 + t1 (s2-s3)/r^3])
+// Target fields other than y live in SMEM, SoA [field][lane] (conflict-free).
+enum NearField { NF_ALPHA = 0, NF_Q0, NF_Q1, NF_Q2, NF_N0, NF_N1, NF_N2, NF_B, NF_W0, NF_W1, NF_W2, kNearFields };
 template <int MODE>
-__device__ __forceinline__ Acc near_pair(const Src& s, const NearTgt& t, const NearParams& p) {
+__device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, double y2,
+                                         const double (*__restrict__ tf)[32], int lane, const NearParams& p,
+                                         const double* __restrict__ tab) {
   Acc a{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  const double dx = t.y0 - s.x, dy = t.y1 - s.y, dz = t.y2 - s.z;
+  const double dx = y0 - s.x, dy = y1 - s.y, dz = y2 - s.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-  double A1, A3, A5, AP;
-  if (r2 < p.r2_tiny) {  // r -> 0 limits (R3)
-    const double i0 = p.inv_delta[0], i1 = p.inv_delta[1], i2 = p.inv_delta[2];
-    A1 = kTwoOverSqrtPi * (t.w0 * i0 + t.w1 * i1 + t.w2 * i2);
-    A3 = (2.0 / 3.0) * kTwoOverSqrtPi * (t.w0 * i0 * i0 * i0 + t.w1 * i1 * i1 * i1 + t.w2 * i2 * i2 * i2);
-    A5 = (4.0 / 15.0) * kTwoOverSqrtPi *
-         (t.w0 * i0 * i0 * i0 * i0 * i0 + t.w1 * i1 * i1 * i1 * i1 * i1 + t.w2 * i2 * i2 * i2 * i2 * i2);
-    AP = A3;
-  } else {
-    const double ri = rsqrt_nr(r2);
-    const double r = r2 * ri;
-    double S1 = 0.0, S2 = 0.0, S3 = 0.0, C = 0.0;
-    const double wk[3] = {t.w0, t.w1, t.w2};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      double s1, s2, s3, c23;
-      s_factors(r * p.inv_delta[k], s1, s2, s3, c23);
-      S1 = fma(wk[k], s1, S1);
-      S2 = fma(wk[k], s2, S2);
-      S3 = fma(wk[k], s3, S3);
-      C = fma(wk[k], c23, C);
-    }
-    const double ri3 = ri * ri * ri;
-    A1 = S1 * ri;
-    A3 = S2 * ri3;
-    A5 = S3 * ri3 * ri * ri;
-    AP = C * ri3;
+  const double ri = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;
+  const double r = r2 * ri;  // 0 for a coincident node
+  // all three deltas through the branch-free table path (independent chains)
+  const double t0 = r * p.inv_delta[0], t1 = r * p.inv_delta[1], t2 = r * p.inv_delta[2];
+  double E0, E1, E2, s20, s21, s22, c0, c1, c2;
+  sfactor_table(t0, tab, E0, s20, c0);
+  sfactor_table(t1, tab, E1, s21, c1);
+  sfactor_table(t2, tab, E2, s22, c2);
+  const double tw0 = tf[NF_W0][lane], tw1 = tf[NF_W1][lane], tw2 = tf[NF_W2][lane];
+  const double w0 = t0 >= 0.5 ? tw0 : 0.0, w1 = t1 >= 0.5 ? tw1 : 0.0, w2 = t2 >= 0.5 ? tw2 : 0.0;
+  const double S1 = fma(w0, E0, fma(w1, E1, w2 * E2));
+  const double S2 = fma(w0, s20, fma(w1, s21, w2 * s22));
+  const double C = fma(w0, c0, fma(w1, c1, w2 * c2));
+  const double S3 = S2 - C;
+  const double ri3 = ri * ri * ri;
+  double A1 = S1 * ri, A3 = S2 * ri3, A5 = S3 * (ri3 * ri * ri), AP = C * ri3;
+  if (t2 < 0.5) {  // rare: r < delta_3 / 2 (t2 is the smallest t)
+    if (t0 < 0.5) sfactor_series_add(t0, p.inv_delta[0], tw0, A1, A3, A5, AP);
+    if (t1 < 0.5) sfactor_series_add(t1, p.inv_delta[1], tw1, A1, A3, A5, AP);
+    sfactor_series_add(t2, p.inv_delta[2], tw2, A1, A3, A5, AP);
   }
   if (MODE & 1) {
-    const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
+    const double alpha = tf[NF_ALPHA][lane];
+    const double gx = fma(-alpha, s.mx, s.fx), gy = fma(-alpha, s.my, s.fy), gz = fma(-alpha, s.mz, s.fz);
     const double dg = fma(dx, gx, fma(dy, gy, dz * gz)) * A3;
     a.u0 = fma(gx, A1, dx * dg);
     a.u1 = fma(gy, A1, dy * dg);
     a.u2 = fma(gz, A1, dz * dg);
   }
   if (MODE & 2) {
-    const double n0 = t.n0, n1 = t.n1, n2 = t.n2, b = t.b;
-    const double qx = s.qx - t.q0, qy = s.qy - t.q1, qz = s.qz - t.q2;
+    const double n0 = tf[NF_N0][lane], n1 = tf[NF_N1][lane], n2 = tf[NF_N2][lane], b = tf[NF_B][lane];
+    const double qx = s.qx - tf[NF_Q0][lane], qy = s.qy - tf[NF_Q1][lane], qz = s.qz - tf[NF_Q2][lane];
     const double dq = fma(dx, qx, fma(dy, qy, dz * qz));
     const double dm = fma(dx, s.mx, fma(dy, s.my, dz * s.mz));
     const double c = dq * dm * A5;
@@ -505,140 +509,166 @@ __device__ __forceinline__ Acc near_pair(const Src& s, const NearTgt& t, const N
   return a;
 }
 
-// K3: near-field pairs.  One warp owns 32 Morton-consecutive targets (lane l
-// accumulates target l).  It finds the 32-source sub-tiles whose box is
-// within c delta_max of its target box, tests the 32 x 32 candidate pairs,
-// compacts the near ones into a target-major list (ballot transpose + warp
-// prefix sum) and evaluates the list 32 pairs at a time with all lanes busy.
-// Each target's results are added in list order: deterministic.
-constexpr int kNearWarps = 4;
 template <int MODE>
-__global__ void __launch_bounds__(kNearWarps * 32) near_kernel(const NearParams p) {
-  __shared__ __align__(16) NearTgt s_tgt[kNearWarps][32];
-  __shared__ __align__(16) double s_src[kNearWarps][32 * kSrcDoubles];
-  __shared__ __align__(16) double s_res[kNearWarps][32][6];
-  __shared__ uint16_t s_list[kNearWarps][32 * 32];
+__device__ __forceinline__ Src load_src_global(const double* __restrict__ g) {
+  const double2* q = reinterpret_cast<const double2*>(g);
+  Src r;
+  double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  r.x = a.x; r.y = a.y; r.z = b.x; r.mx = b.y; r.my = c.x; r.mz = c.y;
+  double2 d = (MODE & 1) ? __ldg(q + 3) : make_double2(0.0, 0.0);
+  double2 e = __ldg(q + 4), f = (MODE & 2) ? __ldg(q + 5) : make_double2(0.0, 0.0);
+  r.fx = d.x; r.fy = d.y; r.fz = e.x;
+  r.qx = e.y; r.qy = f.x; r.qz = f.y;
+  return r;
+}
+
+// K3: near-field pairs.  One warp owns 32 Morton-consecutive targets; lane l
+// owns target l and accumulates it in registers.  The warp walks the 32-source
+// sub-tiles whose box lies within c delta_max of its target box; for each,
+// every lane tests the 32 sources against its target (the same FP64 r^2 as
+// K1's mask, so every pair is counted by exactly one kernel) and appends its
+// near sources to a per-lane ring queue in SMEM.  Whenever every lane holds
+// work, all lanes evaluate one queued pair each per round (no divergence); a
+// lane's pairs are added in discovery order: deterministic.
+constexpr int kNearWarps = 4;
+constexpr int kQCap = 64;  // per-lane ring capacity (power of two)
+#ifndef SER_NEAR_MINB
+#define SER_NEAR_MINB 4
+#endif
+template <int MODE>
+__global__ void __launch_bounds__(kNearWarps * 32, SER_NEAR_MINB) near_kernel(const NearParams p) {
+  __shared__ double s_tab[kErfcxPieces * kErfcxStride];
+  __shared__ double s_sx[kNearWarps][3][32];
+  __shared__ int s_q[kNearWarps][kQCap][32];
+  __shared__ double s_tf[kNearWarps][kNearFields][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t g = (int64_t)blockIdx.x * kNearWarps + warp;  // target group
-  if (g * 32 >= p.Mpad) return;
-  const int64_t ti = g * 32 + lane;
-  {
-    NearTgt t;
-    const double* q = p.tgt + ti;
-    t.y0 = q[F_Y0 * p.Mpad]; t.y1 = q[F_Y1 * p.Mpad]; t.y2 = q[F_Y2 * p.Mpad];
-    t.alpha = q[F_ALPHA * p.Mpad];
-    t.q0 = q[F_Q0 * p.Mpad]; t.q1 = q[F_Q1 * p.Mpad]; t.q2 = q[F_Q2 * p.Mpad];
-    t.n0 = q[F_N0 * p.Mpad]; t.n1 = q[F_N1 * p.Mpad]; t.n2 = q[F_N2 * p.Mpad];
-    t.b = q[F_B * p.Mpad];
-    t.w0 = q[F_W0 * p.Mpad]; t.w1 = q[F_W1 * p.Mpad]; t.w2 = q[F_W2 * p.Mpad];
-    t.pad0 = t.pad1 = 0.0;
-    s_tgt[warp][lane] = t;
-  }
-  double lo[3], hi[3];
-  lo[0] = hi[0] = s_tgt[warp][lane].y0;
-  lo[1] = hi[1] = s_tgt[warp][lane].y1;
-  lo[2] = hi[2] = s_tgt[warp][lane].y2;
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-    for (int o = 16; o; o >>= 1) {
-      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
-      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
-    }
-  __syncwarp();
-  Acc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int i = threadIdx.x; i < kErfcxPieces * kErfcxStride; i += blockDim.x) s_tab[i] = kErfcxTable[i];
+  __syncthreads();
+  int(*q)[32] = s_q[warp];
+  double(*tf)[32] = s_tf[warp];
   const int n_sub = static_cast<int>(p.Npad / kSub);
-  for (int base = 0; base < n_sub; base += 32) {
-    bool mixed = false;
-    const int sb = base + lane;
-    if (sb < n_sub) {
-      const double* bx = p.src_box + (int64_t)sb * 8;
-      double g2 = 0.0;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double gap = fmax(0.0, fmax(bx[d] - hi[d], lo[d] - bx[4 + d]));
-        g2 = fma(gap, gap, g2);
-      }
-      mixed = g2 <= p.rc2_box;
+
+  // persistent warps pull units (group, phase) from a queue: balanced tails
+  for (;;) {
+    int unit = 0;
+    if (lane == 0) unit = atomicAdd(p.counter, 1);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= p.n_units) break;
+    const int64_t g = unit / p.phases;
+    const int phase = unit - static_cast<int>(g) * p.phases;
+    const int64_t ti = g * 32 + lane;
+    const double y0 = p.tgt[F_Y0 * p.Mpad + ti], y1 = p.tgt[F_Y1 * p.Mpad + ti], y2 = p.tgt[F_Y2 * p.Mpad + ti];
+    __syncwarp();
+    {
+      const double* tq = p.tgt + ti;
+      tf[NF_ALPHA][lane] = (MODE & 1) ? tq[F_ALPHA * p.Mpad] : 0.0;
+      tf[NF_Q0][lane] = (MODE & 2) ? tq[F_Q0 * p.Mpad] : 0.0;
+      tf[NF_Q1][lane] = (MODE & 2) ? tq[F_Q1 * p.Mpad] : 0.0;
+      tf[NF_Q2][lane] = (MODE & 2) ? tq[F_Q2 * p.Mpad] : 0.0;
+      tf[NF_N0][lane] = tq[F_N0 * p.Mpad];
+      tf[NF_N1][lane] = tq[F_N1 * p.Mpad];
+      tf[NF_N2][lane] = tq[F_N2 * p.Mpad];
+      tf[NF_B][lane] = tq[F_B * p.Mpad];
+      tf[NF_W0][lane] = tq[F_W0 * p.Mpad];
+      tf[NF_W1][lane] = tq[F_W1 * p.Mpad];
+      tf[NF_W2][lane] = tq[F_W2 * p.Mpad];
     }
-    unsigned mm = __ballot_sync(0xffffffffu, mixed);
-    while (mm) {
-      const int sub = base + __ffs(mm) - 1;
-      mm &= mm - 1;
-      // stage the 32 sources of this sub-tile (lane l loads source l)
-      {
-        const double2* gs = reinterpret_cast<const double2*>(p.src + ((int64_t)sub * kSub + lane) * kSrcDoubles);
-        double2* ds = reinterpret_cast<double2*>(&s_src[warp][lane * kSrcDoubles]);
+    double lo[3] = {y0, y1, y2}, hi[3] = {y0, y1, y2};
 #pragma unroll
-        for (int k = 0; k < kSrcDoubles / 2; ++k) ds[k] = gs[k];
+    for (int d = 0; d < 3; ++d)
+      for (int o = 16; o; o >>= 1) {
+        lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+        hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
       }
-      __syncwarp();
-      // lane l (as source l): which targets are near?
-      const double sx = s_src[warp][lane * kSrcDoubles + 0], sy = s_src[warp][lane * kSrcDoubles + 1],
-                   sz = s_src[warp][lane * kSrcDoubles + 2];
-      unsigned tmask = 0;
-#pragma unroll 8
-      for (int t = 0; t < 32; ++t) {
-        const double dx = s_tgt[warp][t].y0 - sx, dy = s_tgt[warp][t].y1 - sy, dz = s_tgt[warp][t].y2 - sz;
-        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-        tmask |= (r2 <= p.rc2 ? 1u : 0u) << t;
-      }
-      // transpose: lane t gets the mask of its near sources
-      unsigned smask = 0;
-#pragma unroll 8
-      for (int t = 0; t < 32; ++t) {
-        const unsigned b = __ballot_sync(0xffffffffu, (tmask >> t) & 1u);
-        if (lane == t) smask = b;
-      }
-      const int cnt = __popc(smask);
-      int pre = cnt;  // inclusive warp scan
+    Acc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int head = 0, tail = 0;
+    int ordinal = 0;  // index of the mixed sub-tile among this group's mixed sub-tiles
+
+    // Invariant: every lane's queue holds <= kQCap - 32 entries before a sub-tile
+    // appends its (<= 32) near sources.  One call site of the pair code.
+    int base = 0;
+    unsigned mm = 0;
+    for (;;) {
+      while (mm == 0 && base < n_sub) {
+        bool mixed = false;
+        const int sb = base + lane;
+        if (sb < n_sub) {
+          const double* bx = p.src_box + (int64_t)sb * 8;
+          double g2 = 0.0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, pre, 31);
-      const int start = pre - cnt;
-      {  // target-major pair list: (target << 5) | source
-        unsigned m = smask;
-        int pos = start;
+          for (int d = 0; d < 3; ++d) {
+            const double gap = fmax(0.0, fmax(__ldg(bx + d) - hi[d], lo[d] - __ldg(bx + 4 + d)));
+            g2 = fma(gap, gap, g2);
+          }
+          mixed = g2 <= p.rc2_box;
+        }
+        mm = __ballot_sync(0xffffffffu, mixed);
+        // keep only this phase's share of the mixed sub-tiles (round robin by ordinal)
+        unsigned keep = 0, m = mm;
         while (m) {
-          const int sidx = __ffs(m) - 1;
+          const int bit = __ffs(m) - 1;
           m &= m - 1;
-          s_list[warp][pos++] = static_cast<uint16_t>((lane << 5) | sidx);
+          if (ordinal % p.phases == phase) keep |= 1u << bit;
+          ++ordinal;
         }
+        mm = keep;
+        base += 32;
       }
-      __syncwarp();
-      for (int rb = 0; rb < total; rb += 32) {
-        const int pidx = rb + lane;
-        if (pidx < total) {
-          const int code = s_list[warp][pidx];
-          const Src s = load_src<MODE>(&s_src[warp][(code & 31) * kSrcDoubles]);
-          const Acc d = near_pair<MODE>(s, s_tgt[warp][code >> 5], p);
-          s_res[warp][lane][0] = d.u0; s_res[warp][lane][1] = d.u1; s_res[warp][lane][2] = d.u2;
-          s_res[warp][lane][3] = d.v0; s_res[warp][lane][4] = d.v1; s_res[warp][lane][5] = d.v2;
+      int rounds;
+      const bool last = (mm == 0);
+      if (!last) {
+        const int sub = base - 32 + __ffs(mm) - 1;
+        mm &= mm - 1;
+        {
+          const double* gs = p.src + ((int64_t)sub * kSub + lane) * kSrcDoubles;
+          s_sx[warp][0][lane] = __ldg(gs);
+          s_sx[warp][1][lane] = __ldg(gs + 1);
+          s_sx[warp][2][lane] = __ldg(gs + 2);
         }
         __syncwarp();
-        // lane t adds its own entries of this round, in list order
-        const int lo_i = max(start, rb), hi_i = min(start + cnt, rb + 32);
-        for (int k = lo_i; k < hi_i; ++k) {
-          const double* r = s_res[warp][k - rb];
-          acc.u0 += r[0]; acc.u1 += r[1]; acc.u2 += r[2];
-          acc.v0 += r[3]; acc.v1 += r[4]; acc.v2 += r[5];
+        unsigned smask = 0;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+          const double dx = y0 - s_sx[warp][0][k], dy = y1 - s_sx[warp][1][k], dz = y2 - s_sx[warp][2][k];
+          const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+          smask |= (r2 <= p.rc2 ? 1u : 0u) << k;
         }
         __syncwarp();
+        while (smask) {
+          const int bit = __ffs(smask) - 1;
+          smask &= smask - 1;
+          q[tail & (kQCap - 1)][lane] = sub * kSub + bit;
+          ++tail;
+        }
+        const int minlen = __reduce_min_sync(0xffffffffu, tail - head);
+        const int maxlen = __reduce_max_sync(0xffffffffu, tail - head);
+        rounds = max(minlen >= 32 ? minlen : 0, maxlen - (kQCap - 32));
+      } else {
+        rounds = __reduce_max_sync(0xffffffffu, tail - head);  // drain
       }
+      for (int r = 0; r < rounds; ++r) {
+        if (head < tail) {
+          const int sidx = q[head & (kQCap - 1)][lane];
+          ++head;
+          const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
+          const Acc d = near_pair<MODE>(s, y0, y1, y2, tf, lane, p, s_tab);
+          acc.u0 += d.u0; acc.u1 += d.u1; acc.u2 += d.u2;
+          acc.v0 += d.v0; acc.v1 += d.v1; acc.v2 += d.v2;
+        }
+      }
+      if (last) break;
     }
+    double* out = p.near_out + (int64_t)phase * 6 * p.Mpad + ti;
+    out[0 * p.Mpad] = acc.u0; out[1 * p.Mpad] = acc.u1; out[2 * p.Mpad] = acc.u2;
+    out[3 * p.Mpad] = acc.v0; out[4 * p.Mpad] = acc.v1; out[5 * p.Mpad] = acc.v2;
   }
-  double* out = p.near_out + ti;
-  out[0 * p.Mpad] = acc.u0; out[1 * p.Mpad] = acc.u1; out[2 * p.Mpad] = acc.u2;
-  out[3 * p.Mpad] = acc.v0; out[4 * p.Mpad] = acc.v1; out[5 * p.Mpad] = acc.v2;
 }
 
 // ------------------------------------------------------------ K2: finalize
 template <int MODE>
 __global__ void finalize_kernel(const double* __restrict__ partial, const double* __restrict__ near_out,
                                 const double* __restrict__ tgt, const int32_t* __restrict__ orig, int64_t M,
-                                int64_t Mpad, int n_chunks, int TB, double* __restrict__ out_u,
+                                int64_t Mpad, int n_chunks, int TB, int phases, double* __restrict__ out_u,
                                 double* __restrict__ out_v) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= M) return;
@@ -650,9 +680,10 @@ __global__ void finalize_kernel(const double* __restrict__ partial, const double
     for (int c = 0; c < 6; ++c)
       if ((c < 3 && (MODE & 1)) || (c >= 3 && (MODE & 2))) s[c] += pp[c * TB];
   }
+  for (int ph = 0; ph < phases; ++ph)
 #pragma unroll
-  for (int c = 0; c < 6; ++c)
-    if ((c < 3 && (MODE & 1)) || (c >= 3 && (MODE & 2))) s[c] += near_out[c * Mpad + i];
+    for (int c = 0; c < 6; ++c)
+      if ((c < 3 && (MODE & 1)) || (c >= 3 && (MODE & 2))) s[c] += near_out[((int64_t)ph * 6 + c) * Mpad + i];
   const int64_t o = orig[i];
   const double inv8pi = 1.0 / (8.0 * kPi);
   if (MODE & 1)

@@ -123,7 +123,7 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct Plan {
   int mode = 3, T = 2;
   int64_t M = 0, N = 0, Mpad = 0, Npad = 0;
-  int n_tiles = 0, n_tblocks = 0, chunk_tiles = 0, n_chunks = 0, n_items = 0;
+  int n_tiles = 0, n_tblocks = 0, chunk_tiles = 0, n_chunks = 0, n_items = 0, near_phases = 1;
   size_t cub_bytes = 0;
   size_t off_box, off_skin, off_skout, off_svin, off_svout, off_tkin, off_tkout, off_tvin, off_tvout;
   size_t off_cub, off_src, off_srcbox, off_tgt, off_orig, off_partial, off_near, off_counter, total;
@@ -140,7 +140,7 @@ size_t cub_sort_bytes(int64_t n) {
 Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override) {
   Plan p;
   p.mode = mode;
-  p.T = (T == 4) ? 4 : 2;
+  p.T = (T == 3 || T == 4) ? T : 2;
   p.M = M;
   p.N = N;
   p.Npad = ceil_div(N, kTile) * kTile;
@@ -180,7 +180,10 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override) {
   p.off_tgt = take(p.Mpad * kTgtFields * sizeof(double));
   p.off_orig = take(p.Mpad * sizeof(int32_t));
   p.off_partial = take((size_t)p.n_items * 6 * TB * sizeof(double));
-  p.off_near = take((size_t)p.Mpad * 6 * sizeof(double));
+  // near units (32-target group, phase): >= ~4 per resident warp (148 SMs x 12 warps)
+  const int64_t groups = p.Mpad / 32;
+  p.near_phases = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(4 * 148 * 12, groups))));
+  p.off_near = take((size_t)p.near_phases * p.Mpad * 6 * sizeof(double));
   p.off_counter = take(sizeof(int) * 4);
   p.total = off;
   return p;
@@ -259,7 +262,7 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox);
   Delta3 r3{{rho[0], rho[1], rho[2]}};
   pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, tgt, orig);
-  if (cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
+  if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
 
   PairParams pp;
   pp.src = src;
@@ -282,6 +285,7 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
     cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
   int grid = 0;
   if (P.T == 4) launch_pairs<MODE, 4>(pp, s, &grid);
+  else if (P.T == 3) launch_pairs<MODE, 3>(pp, s, &grid);
   else launch_pairs<MODE, 2>(pp, s, &grid);
   if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
 
@@ -290,6 +294,9 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   np.src_box = srcbox;
   np.tgt = tgt;
   np.near_out = near_out;
+  np.counter = counter + 1;
+  np.phases = P.near_phases;
+  np.n_units = static_cast<int>((P.Mpad / 32) * P.near_phases);
   np.Mpad = P.Mpad;
   np.Npad = P.Npad;
   np.rc2 = pp.rc2;
@@ -298,7 +305,15 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = pp.inv_delta[k];
   if (opt && opt->near_kernel_start_event)
     cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_start_event), s);
-  near_kernel<MODE><<<ceil_div(P.Mpad / 32, kNearWarps), kNearWarps * 32, 0, s>>>(np);
+  {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_kernel<MODE>, kNearWarps * 32, 0);
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(occ, 1))));
+    near_kernel<MODE><<<grid, kNearWarps * 32, 0, s>>>(np);
+  }
   if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
   if (opt) {
     opt->stats[0] = P.n_items;
@@ -307,11 +322,13 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
     opt->stats[3] = P.T;
   }
   finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad, P.n_chunks,
-                                                          kThreads * P.T, out_u, out_v);
+                                                          kThreads * P.T, P.near_phases, out_u, out_v);
   return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
 }
 
-int opt_T(const stokes_er_options* o) { return (o && o->targets_per_thread == 4) ? 4 : 2; }
+int opt_T(const stokes_er_options* o) {
+  return (o && (o->targets_per_thread == 3 || o->targets_per_thread == 4)) ? o->targets_per_thread : 2;
+}
 int opt_chunk(const stokes_er_options* o) { return o ? o->source_chunk_tiles : 0; }
 
 size_t host_stage_bytes(int64_t M, int64_t N) {
@@ -326,7 +343,8 @@ extern "C" {
 size_t stokes_er_workspace_bytes(int64_t M, int64_t N, int mode) {
   if (M < 0 || N < 1 || mode < 1 || mode > 3) return 0;
   // the larger of the two tunings, so one workspace serves every option
-  return std::max(make_plan(M, N, mode, 2, 0).total, make_plan(M, N, mode, 4, 0).total);
+  return std::max({make_plan(M, N, mode, 2, 0).total, make_plan(M, N, mode, 3, 0).total,
+                   make_plan(M, N, mode, 4, 0).total});
 }
 
 size_t stokes_er_workspace_bytes_ex(int64_t M, int64_t N, int mode, const stokes_er_options* options) {
