@@ -265,11 +265,8 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     pair_ms = [a.elapsed_time(b) for a, b in evp]
     near_ms = [a.elapsed_time(b) for a, b in evn]
-    total_s = sum(step_ms) / 1e3
-    if dist is not None:
-        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_s = float(t.item())
+    from paper_2507_00156_b200.sharding import max_over_ranks
+    total_s = max_over_ranks(sum(step_ms) / 1e3, dev)
     value = world * pairs * K / total_s
 
     # end-to-end through the C ABI with pinned HOST buffers (copies inside the timed region)
@@ -294,11 +291,7 @@ def main():
             b.record(stream)
             b.synchronize()
             e_ms.append(a.elapsed_time(b))
-        e_total = sum(e_ms) / 1e3
-        if dist is not None:
-            t = torch.tensor([e_total], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_total = float(t.item())
+        e_total = max_over_ranks(sum(e_ms) / 1e3, dev)
         e2e = {"value": world * pairs * ke / e_total, "unit": UNIT,
                "h2d_bytes_per_step": int(sum(a.nbytes for a in block.arrays())),
                "d2h_bytes_per_step": int(hu.numel() * 8 + hv.numel() * 8)}

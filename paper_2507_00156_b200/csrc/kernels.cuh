@@ -33,7 +33,10 @@
 
 namespace ser {
 
-constexpr int kThreads = 128;        // threads per pair-kernel CTA (4 warps)
+#ifndef SER_FAR_THREADS
+#define SER_FAR_THREADS 128
+#endif
+constexpr int kThreads = SER_FAR_THREADS;  // threads per far-kernel CTA (tuning macro)
 #ifndef SER_TILE
 #define SER_TILE 128
 #endif
@@ -42,7 +45,6 @@ constexpr int kSub = 32;             // sources per classification sub-tile
 constexpr int kSrcDoubles = 12;      // packed source record: x(3) mw(3) fw(3) q(3)
 constexpr int kTgtFields = 14;       // y(3) alpha q0(3) n0(3) b w(3)
 constexpr int kTileBytes = kTile * kSrcDoubles * 8;
-constexpr int kNominalCtas = 148 * 3;  // plan assumption
 constexpr double kPartialCapBytes = 256.0 * 1024 * 1024;
 
 enum TgtField { F_Y0 = 0, F_Y1, F_Y2, F_ALPHA, F_Q0, F_Q1, F_Q2, F_N0, F_N1, F_N2, F_B, F_W0, F_W1, F_W2 };
@@ -275,12 +277,35 @@ struct Acc {
 // Far pair: unregularized Stokeslet (eq. 3) on g = f w - alpha m w and stresslet
 // (eq. 4) on dq = q - q0 contracted with m w; the -6
 // and 1/(8pi) are applied once in the finalize.  41 FP64 instructions (BOTH).
+#ifndef SER_FAR_V2
+#define SER_FAR_V2 0
+#endif
 template <int MODE>
 __device__ __forceinline__ void far_pair(const Src& s, const Tgt& t, Acc& a) {
   const double dx = t.y0 - s.x, dy = t.y1 - s.y, dz = t.y2 - s.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   const double ri = rsqrt_nr(r2);
   const double ri2 = ri * ri;
+#if SER_FAR_V2
+  if (MODE == 3) {
+    // dot products with d interleaved component-wise: consecutive DFMAs share
+    // their first operand (register-reuse friendly)
+    const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
+    const double qx = s.qx - t.q0, qy = s.qy - t.q1, qz = s.qz - t.q2;
+    double pg = dz * gz, pq = dz * qz, pm = dz * s.mz;
+    pg = fma(dy, gy, pg); pq = fma(dy, qy, pq); pm = fma(dy, s.my, pm);
+    pg = fma(dx, gx, pg); pq = fma(dx, qx, pq); pm = fma(dx, s.mx, pm);
+    const double a3 = pg * ri2;
+    const double c = (pq * pm) * (ri2 * ri2 * ri);
+    a.u0 = fma(fma(dx, a3, gx), ri, a.u0);
+    a.u1 = fma(fma(dy, a3, gy), ri, a.u1);
+    a.u2 = fma(fma(dz, a3, gz), ri, a.u2);
+    a.v0 = fma(dx, c, a.v0);
+    a.v1 = fma(dy, c, a.v1);
+    a.v2 = fma(dz, c, a.v2);
+    return;
+  }
+#endif
   if (MODE & 1) {
     const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
     const double a3 = fma(dx, gx, fma(dy, gy, dz * gz)) * ri2;
@@ -331,7 +356,10 @@ __device__ __forceinline__ void far_pair_masked(const Src& s, const Tgt& t, Acc&
 // source chunk) items from a queue; each item's partial sums go to their own
 // slot, summed in fixed order by the finalize (deterministic).
 template <int MODE, int T>
-__global__ void __launch_bounds__(kThreads) far_kernel(const PairParams p) {
+#ifndef SER_FAR_MINB
+#define SER_FAR_MINB (512 / SER_FAR_THREADS)
+#endif
+__global__ void __launch_bounds__(kThreads, SER_FAR_MINB) far_kernel(const PairParams p) {
   __shared__ __align__(128) double tile[2][kTile * kSrcDoubles];
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int s_item;

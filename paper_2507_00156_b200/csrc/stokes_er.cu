@@ -150,9 +150,11 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override) {
   p.Mpad = (int64_t)p.n_tblocks * TB;
   // work items (target block, source chunk): >= 16 per nominal CTA slot so the
   // dynamic queue's tail is small, each >= 4 tiles, partials <= 256 MB.
-  int64_t want = ceil_div(16 * kNominalCtas, p.n_tblocks);
+  const int64_t nominal_ctas = 148 * (16 * 32 / kThreads);  // 16 resident warps per SM
+  int64_t want = ceil_div(16 * nominal_ctas, p.n_tblocks);
   const int64_t mem_cap = std::max<int64_t>(1, (int64_t)(kPartialCapBytes / (48.0 * (double)p.Mpad)));
-  const int64_t max_chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.n_tiles, 4), mem_cap));
+  const int64_t min_tiles = std::max(1, 512 / kTile);  // >= 512 sources per item
+  const int64_t max_chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.n_tiles, min_tiles), mem_cap));
   want = std::min<int64_t>(std::max<int64_t>(want, 1), max_chunks);
   p.chunk_tiles = static_cast<int>(ceil_div(p.n_tiles, want));
   if (chunk_override > 0) p.chunk_tiles = std::min(chunk_override, p.n_tiles);

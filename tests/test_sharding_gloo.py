@@ -1,0 +1,78 @@
+"""N > 1 host logic on CPU: world_size-2 gloo processes shard the targets, evaluate
+their range (the CPU oracle stands in for the CUDA evaluator: no GPU here) and
+all-gather; the result must equal the single-process evaluation bit for bit."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2507_00156_b200.sharding import shard_bounds
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_shard_bounds_partition():
+    for M in (0, 1, 7, 504, 1001):
+        for world in (1, 2, 3, 8):
+            rngs = [shard_bounds(M, r, world) for r in range(world)]
+            assert rngs[0][0] == 0 and rngs[-1][1] == M
+            assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
+            sizes = [b - a for a, b in rngs]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2507_00156_b200.sharding import evaluate_sharded, max_over_ranks
+    from workloads.configs import config1
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    blk = config1(inv_h=8, per_class=11)  # M = 77: uneven shards
+
+    def oracle_fn(sx, sn, sw, f, q, ty, tb, tx, h, rho, mode=3):
+        u, v = oracle.evaluate(*(a.numpy() for a in (sx, sn, sw, f, q, ty, tb, tx)), h, rho, mode=mode)
+        return torch.from_numpy(u), torch.from_numpy(v)
+
+    arrs = [torch.from_numpy(a) for a in blk.arrays()]
+    u, v = evaluate_sharded(*arrs, blk.h, blk.rho, evaluate_fn=oracle_fn)
+    t = max_over_ranks(1.0 + rank)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "u.npy"), u.numpy())
+        np.save(os.path.join(out_dir, "v.npy"), v.numpy())
+        np.save(os.path.join(out_dir, "t.npy"), np.array([t]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_shard_and_gather(tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle
+    from workloads.configs import config1
+
+    oracle.build()
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    blk = config1(inv_h=8, per_class=11)
+    u_ref, v_ref = oracle.evaluate_block(blk)
+    np.testing.assert_array_equal(np.load(tmp_path / "u.npy"), u_ref)
+    np.testing.assert_array_equal(np.load(tmp_path / "v.npy"), v_ref)
+    assert float(np.load(tmp_path / "t.npy")[0]) == 2.0  # max over ranks

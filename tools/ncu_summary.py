@@ -1,0 +1,55 @@
+#!/usr/bin/env python
+"""Summarise an ncu report (.ncu-rep) into profiles/: key metrics per kernel as JSON.
+
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01/ncu_xxx.json
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", "smsp__inst_executed.sum",
+    "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
+    "launch__block_size", "launch__shared_mem_per_block_static", "sm__cycles_elapsed.avg.per_second",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "lts__t_sector_hit_rate.pct", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+]
+STALL_PREFIX = "smsp__average_warps_issue_stalled_"
+
+
+def main(rep, out):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for row in rows[2:]:
+        k = {"kernel": row[hdr.index("Kernel Name")]}
+        for i, name in enumerate(hdr):
+            if name in KEYS:
+                k[name] = f"{row[i]} {units[i]}".strip()
+            elif name.startswith(STALL_PREFIX) and name.endswith("_per_issue_active.ratio"):
+                v = row[i]
+                try:
+                    if float(v) > 0.01:
+                        k.setdefault("stalls_per_issue", {})[name[len(STALL_PREFIX):-len("_per_issue_active.ratio")]] = float(v)
+                except ValueError:
+                    pass
+        res.append(k)
+    with open(out, "w") as fh:
+        json.dump({"report": rep, "kernels": res}, fh, indent=1)
+    print(json.dumps(res, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])
