@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
+    ap.add_argument("--near-phases", type=int, default=0)
     return ap.parse_args()
 
 
@@ -224,6 +225,8 @@ def main():
     opt = ser.Options()
     if args.targets_per_thread:
         opt.targets_per_thread = args.targets_per_thread
+    if args.near_phases:
+        opt.near_phases = args.near_phases
     nbytes = int(ser._lib.load().stokes_er_workspace_bytes_ex(M, N, 3, __import__("ctypes").byref(opt)))
     ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)

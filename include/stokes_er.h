@@ -143,11 +143,12 @@ int stokes_er_launch_count(int64_t M, int64_t N, int mode);
 typedef struct {
   void* pair_kernel_start_event;
   void* pair_kernel_end_event;
-  int targets_per_thread; /* 0 = default (2); 2, 3 or 4 (tuning/tests)    */
+  int targets_per_thread; /* 0 = default (2); 1..4 (tuning/tests)         */
   int source_chunk_tiles; /* 0 = automatic; work item = chunk * 128 sources */
   int64_t stats[4];       /* out: [0] work items, [1] grid CTAs, [2] chunk tiles, [3] targets/thread */
   void* near_kernel_start_event; /* optional events around the near-field kernel */
   void* near_kernel_end_event;
+  int near_phases;               /* 0 = automatic; near work units per 32-target group (1..64) */
 } stokes_er_options;
 
 /* Workspace for stokes_er_eval_ex with these tuning options (>= stokes_er_workspace_bytes

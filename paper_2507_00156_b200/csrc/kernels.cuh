@@ -37,6 +37,10 @@ namespace ser {
 #define SER_FAR_THREADS 128
 #endif
 constexpr int kThreads = SER_FAR_THREADS;  // threads per far-kernel CTA (tuning macro)
+#ifndef SER_FAR_UNROLL
+#define SER_FAR_UNROLL 2
+#endif
+constexpr int kFarUnroll = SER_FAR_UNROLL;  // sources per all-far loop iteration (tuning macro)
 #ifndef SER_TILE
 #define SER_TILE 128
 #endif
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) far_kernel(const PairP
         }
         const double* ss = sm + sub * kSub * kSrcDoubles;
         if (g2 > p.rc2_box) {  // warp-uniform: every pair of this sub-tile is far
-#pragma unroll 2
+#pragma unroll kFarUnroll
           for (int k = 0; k < kSub; ++k) {
             const Src s = load_src<MODE>(ss + k * kSrcDoubles);
 #pragma unroll

@@ -137,10 +137,10 @@ size_t cub_sort_bytes(int64_t n) {
   return bytes;
 }
 
-Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override) {
+Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override, int phases_override = 0) {
   Plan p;
   p.mode = mode;
-  p.T = (T == 3 || T == 4) ? T : 2;
+  p.T = (T >= 1 && T <= 4) ? T : 2;
   p.M = M;
   p.N = N;
   p.Npad = ceil_div(N, kTile) * kTile;
@@ -184,7 +184,8 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override) {
   p.off_partial = take((size_t)p.n_items * 6 * TB * sizeof(double));
   // near units (32-target group, phase): >= ~4 per resident warp (148 SMs x 12 warps)
   const int64_t groups = p.Mpad / 32;
-  p.near_phases = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(4 * 148 * 12, groups))));
+  p.near_phases = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));
+  if (phases_override > 0) p.near_phases = std::min(phases_override, 64);
   p.off_near = take((size_t)p.near_phases * p.Mpad * 6 * sizeof(double));
   p.off_counter = take(sizeof(int) * 4);
   p.total = off;
@@ -288,6 +289,7 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   int grid = 0;
   if (P.T == 4) launch_pairs<MODE, 4>(pp, s, &grid);
   else if (P.T == 3) launch_pairs<MODE, 3>(pp, s, &grid);
+  else if (P.T == 1) launch_pairs<MODE, 1>(pp, s, &grid);
   else launch_pairs<MODE, 2>(pp, s, &grid);
   if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
 
@@ -329,9 +331,10 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
 }
 
 int opt_T(const stokes_er_options* o) {
-  return (o && (o->targets_per_thread == 3 || o->targets_per_thread == 4)) ? o->targets_per_thread : 2;
+  return (o && o->targets_per_thread >= 1 && o->targets_per_thread <= 4) ? o->targets_per_thread : 2;
 }
 int opt_chunk(const stokes_er_options* o) { return o ? o->source_chunk_tiles : 0; }
+int opt_phases(const stokes_er_options* o) { return o ? o->near_phases : 0; }
 
 size_t host_stage_bytes(int64_t M, int64_t N) {
   return align_up(13 * N * sizeof(double)) + align_up(13 * M * sizeof(double)) + align_up(6 * M * sizeof(double)) +
@@ -345,14 +348,14 @@ extern "C" {
 size_t stokes_er_workspace_bytes(int64_t M, int64_t N, int mode) {
   if (M < 0 || N < 1 || mode < 1 || mode > 3) return 0;
   // the larger of the two tunings, so one workspace serves every option
-  return std::max({make_plan(M, N, mode, 2, 0).total, make_plan(M, N, mode, 3, 0).total,
-                   make_plan(M, N, mode, 4, 0).total});
+  return std::max({make_plan(M, N, mode, 1, 0).total, make_plan(M, N, mode, 2, 0).total,
+                   make_plan(M, N, mode, 3, 0).total, make_plan(M, N, mode, 4, 0).total});
 }
 
 size_t stokes_er_workspace_bytes_ex(int64_t M, int64_t N, int mode, const stokes_er_options* options) {
   if (M < 0 || N < 1 || mode < 1 || mode > 3) return 0;
   return std::max(stokes_er_workspace_bytes(M, N, mode),
-                  make_plan(M, N, mode, opt_T(options), opt_chunk(options)).total);
+                  make_plan(M, N, mode, opt_T(options), opt_chunk(options), opt_phases(options)).total);
 }
 
 int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const double* src_weight,
@@ -365,7 +368,7 @@ int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const dou
   if (M == 0) return STOKES_ER_OK;
   if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
   if ((st = check_arch())) return st;
-  const Plan P = make_plan(M, N, mode, opt_T(options), opt_chunk(options));
+  const Plan P = make_plan(M, N, mode, opt_T(options), opt_chunk(options), opt_phases(options));
   if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(workspace);
