@@ -55,6 +55,8 @@ extern "C" {
 #define STOKES_ER_ABI_VERSION 1
 /* c: near iff r <= c * max(delta_k)  ("s1=s2=s3=1 for t > 6") */
 #define STOKES_ER_CUTOFF 6.0
+/* c for the on-surface s# variant: 1 - s2#(6) = 2.45e-12, 1 - s_i#(7) < 1e-16 (R15) */
+#define STOKES_ER_CUTOFF_SURFACE 7.0
 
 typedef enum {
   STOKES_ER_SL = 1,   /* single layer only: f required, out_u written            */
@@ -133,6 +135,22 @@ int stokes_er_eval_deltas(const double* src_xyz, const double* src_normal, const
  */
 int stokes_er_extrapolate(const double* tgt_b, int64_t M, double h, const double rho[3],
                           const double* in_delta, int C, double* out, void* stream);
+
+/*
+ * NEXT-1: on-surface evaluation with the modified factors s1#, s2#, s3# of
+ * PAPER.md Sec. 2.1 (lines 126-139) at ONE smoothing length delta (the
+ * paper uses delta = 3h for self-surface integrals), no
+ * extrapolation.  SL: S^delta of eq. (12) with s1#, s2#; DL: the unsplit
+ * stresslet eq. (4) times s3# (R16) plus chi q(x0).  Near iff
+ * r <= STOKES_ER_CUTOFF_SURFACE * delta.  Same arrays, workspace
+ * (stokes_er_workspace_bytes) and error behaviour as stokes_er_eval;
+ * intended for targets on the surface (b = 0, chi = 1/2).
+ */
+int stokes_er_eval_onsurface(const double* src_xyz, const double* src_normal, const double* src_weight,
+                             const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                             const double* tgt_x0_density, int64_t M, int64_t N, double delta, int mode,
+                             double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
+                             void* stream);
 
 /* Number of kernel launches one stokes_er_eval(M, N, mode) enqueues. */
 int stokes_er_launch_count(int64_t M, int64_t N, int mode);

@@ -197,12 +197,21 @@ static void eval_target(const double* src_xyz, const double* src_normal, const d
             double S = (i == a ? A[0] : 0.0) + yh[i] * yh[a] * A[1];  /* eq. (12) */
             nadd(&Us[k][i], S * g[a] * w);
           }
-      if (mode & 2)
+      if ((mode & 2) && !sharp)
         for (int i = 0; i < 3; ++i)
           for (int a = 0; a < 3; ++a)
             for (int c = 0; c < 3; ++c) {
               /* T^d = T1 s2 + T2 s3 (eq. 13) with T1, T2 of eq. (7) */
               double T = -6.0 * (t1[i][a][c] * A[1] + (t2[i][a][c] - (r2 - b * b) * t1[i][a][c]) * A[2]);
+              nadd(&Vs[k][i], T * dq[a] * m[c] * w);
+            }
+      if ((mode & 2) && sharp)
+        for (int i = 0; i < 3; ++i)
+          for (int a = 0; a < 3; ++a)
+            for (int c = 0; c < 3; ++c) {
+              /* reading R16: on the surface the stresslet is regularized unsplit,
+               * T# = T s3#(r/d) = -6 yh_i yh_a yh_c s3#/r^5 (eq. 4 times s3#) */
+              double T = -6.0 * yh[i] * yh[a] * yh[c] * A[2];
               nadd(&Vs[k][i], T * dq[a] * m[c] * w);
             }
     }

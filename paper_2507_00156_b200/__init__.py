@@ -18,6 +18,7 @@ from . import _lib
 
 SL, DL, BOTH = 1, 2, 3
 CUTOFF = 6.0  # STOKES_ER_CUTOFF
+CUTOFF_SURFACE = 7.0  # STOKES_ER_CUTOFF_SURFACE (R15)
 
 
 def _torch():
@@ -137,6 +138,27 @@ def evaluate_host(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_
         _ptr(q if mode & DL else None), _ptr(tgt_xyz), _ptr(tgt_b), _ptr(tgt_x0_density), M, N, float(h),
         _lib.rho_arg(rho), int(mode), _ptr(out_u if mode & SL else None), _ptr(out_v if mode & DL else None),
         _ptr(workspace), int(workspace.numel()), _stream_handle(stream)))
+    return (out_u if mode & SL else None), (out_v if mode & DL else None)
+
+
+def evaluate_onsurface(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, delta, mode=BOTH,
+                       out_u=None, out_v=None, workspace=None, stream=None):
+    """stokes_er_eval_onsurface (NEXT-1): single delta, s# factors, no extrapolation."""
+    torch = _torch()
+    M, N = _shapes(src_xyz, tgt_b)
+    dev = src_xyz.device
+    if mode & SL and out_u is None:
+        out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    if mode & DL and out_v is None:
+        out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+    if workspace is None:
+        workspace = alloc_workspace(M, N, mode, dev)
+    L = _lib.load()
+    _lib.check("stokes_er_eval_onsurface", L.stokes_er_eval_onsurface(
+        _ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
+        _ptr(q if mode & DL else None), _ptr(tgt_xyz), _ptr(tgt_b), _ptr(tgt_x0_density), M, N, float(delta),
+        int(mode), _ptr(out_u if mode & SL else None), _ptr(out_v if mode & DL else None), _ptr(workspace),
+        int(workspace.numel()), _stream_handle(stream)))
     return (out_u if mode & SL else None), (out_v if mode & DL else None)
 
 

@@ -31,7 +31,7 @@ class Options(ctypes.Structure):
 
 
 EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_er_eval", "stokes_er_eval_ex", "stokes_er_host_workspace_bytes",
-           "stokes_er_eval_host", "stokes_er_eval_deltas", "stokes_er_extrapolate", "stokes_er_launch_count",
+           "stokes_er_eval_host", "stokes_er_eval_deltas", "stokes_er_eval_onsurface", "stokes_er_extrapolate", "stokes_er_launch_count",
            "stokes_er_status_string", "stokes_er_abi_version"]
 
 _lib = None
@@ -60,6 +60,9 @@ def load():
     L.stokes_er_eval_ex.restype = ctypes.c_int
     L.stokes_er_eval_host.argtypes = eval_args
     L.stokes_er_eval_host.restype = ctypes.c_int
+    L.stokes_er_eval_onsurface.argtypes = [_dp] * 8 + [_i64, _i64, ctypes.c_double, ctypes.c_int, _dp, _dp, _dp,
+                                                      ctypes.c_size_t, _dp]
+    L.stokes_er_eval_onsurface.restype = ctypes.c_int
     L.stokes_er_eval_deltas.argtypes = eval_args
     L.stokes_er_eval_deltas.restype = ctypes.c_int
     L.stokes_er_extrapolate.argtypes = [_dp, _i64, ctypes.c_double, ctypes.POINTER(ctypes.c_double), _dp,

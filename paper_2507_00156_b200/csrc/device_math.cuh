@@ -145,4 +145,40 @@ __device__ __forceinline__ void sfactor_series_add(double t, double invd, double
   AP = fma(wi3, (2.0 / 3.0) * kTwoOverSqrtPi * exp_neg(u), AP);  // (4/(3 sqrt pi)) e^{-t^2}
 }
 
+// NEXT-1 on-surface factors at one delta, t = r/delta:
+//   t >= 0.5: s1# = E + (2/(3 sqrt pi))(5t - 2t^3) e, s2# = E - (2/(3 sqrt pi))(3t - 14t^3 + 4t^5) e,
+//             s3# = E - (2/(9 sqrt pi))(9t + 6t^3 - 4t^5) e   (E, e from the same table/exp path)
+//   t <  0.5: s#/t, s#/t^3, s#/t^5 from their series (coefficients generated and self-checked).
+// Returns A1 = s1#/r, A3 = s2#/r^3, A5 = s3#/r^5.
+__device__ __forceinline__ void sharp_weights(double r, double ri, double invd, const double* __restrict__ tab,
+                                              double& A1, double& A3, double& A5) {
+  const double t = r * invd;
+  if (t < 0.5) {
+    const double u = t * t;
+    double f1 = kPhi1S[kSeriesTerms - 1], f3 = kPhi3S[kSeriesTerms - 1], f5 = kPhi5S[kSeriesTerms - 1];
+#pragma unroll
+    for (int j = kSeriesTerms - 2; j >= 0; --j) {
+      f1 = fma(f1, u, kPhi1S[j]);
+      f3 = fma(f3, u, kPhi3S[j]);
+      f5 = fma(f5, u, kPhi5S[j]);
+    }
+    const double i3 = invd * invd * invd;
+    A1 = f1 * invd;
+    A3 = f3 * i3;
+    A5 = f5 * i3 * invd * invd;
+    return;
+  }
+  double E, s2, c23;
+  sfactor_table(t, tab, E, s2, c23);
+  const double e = exp_neg(t * t) * kInvSqrtPi;  // e^{-t^2}/sqrt(pi)
+  const double t2 = t * t, t3 = t2 * t, t5 = t3 * t2;
+  const double s1s = fma((2.0 / 3.0) * e, fma(-2.0, t3, 5.0 * t), E);
+  const double s2s = fma(-(2.0 / 3.0) * e, fma(4.0, t5, fma(-14.0, t3, 3.0 * t)), E);
+  const double s3s = fma(-(2.0 / 9.0) * e, fma(-4.0, t5, fma(6.0, t3, 9.0 * t)), E);
+  const double ri3 = ri * ri * ri;
+  A1 = s1s * ri;
+  A3 = s2s * ri3;
+  A5 = s3s * ri3 * ri * ri;
+}
+
 }  // namespace ser

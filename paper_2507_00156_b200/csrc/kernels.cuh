@@ -217,8 +217,8 @@ struct Delta3 {
 template <int MODE>
 __global__ void pack_targets(const double* __restrict__ xyz, const double* __restrict__ tb,
                              const double* __restrict__ x0d, int64_t M, int64_t Mpad,
-                             const int32_t* __restrict__ perm, double h, Delta3 rho, double* __restrict__ tgt,
-                             int32_t* __restrict__ orig) {
+                             const int32_t* __restrict__ perm, double h, Delta3 rho, bool sharp,
+                             double* __restrict__ tgt, int32_t* __restrict__ orig) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= Mpad) return;
   const int64_t j = perm[i < M ? i : M - 1];
@@ -230,8 +230,8 @@ __global__ void pack_targets(const double* __restrict__ xyz, const double* __res
     f0[d] = (MODE & 1) ? x0d[(3 + d) * M + j] : 0.0;
     q0[d] = (MODE & 2) ? x0d[(6 + d) * M + j] : 0.0;
   }
-  double w[3];
-  extrap_weights(b, h, rho.rho, STOKES_ER_CUTOFF, w);
+  double w[3] = {1.0, 0.0, 0.0};  // NEXT-1: a single delta, no extrapolation
+  if (!sharp) extrap_weights(b, h, rho.rho, STOKES_ER_CUTOFF, w);
   tgt[F_Y0 * Mpad + i] = xyz[j];
   tgt[F_Y1 * Mpad + i] = xyz[M + j];
   tgt[F_Y2 * Mpad + i] = xyz[2 * M + j];
@@ -483,7 +483,7 @@ struct NearTgt {
 //       eq. 7 rearranged: T1 s2 + T2 s3 = -6[yyy s3/r^5 + t1 (s2-s3)/r^3])
 // Target fields other than y live in SMEM, SoA [field][lane] (conflict-free).
 enum NearField { NF_ALPHA = 0, NF_Q0, NF_Q1, NF_Q2, NF_N0, NF_N1, NF_N2, NF_B, NF_W0, NF_W1, NF_W2, kNearFields };
-template <int MODE>
+template <int MODE, bool SHARP>
 __device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, double y2,
                                          const double (*__restrict__ tf)[32], int lane, const NearParams& p,
                                          const double* __restrict__ tab) {
@@ -492,6 +492,26 @@ __device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, dou
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   const double ri = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;
   const double r = r2 * ri;  // 0 for a coincident node
+  if (SHARP) {  // NEXT-1: one delta, s# factors, unsplit stresslet (R16)
+    double A1, A3, A5;
+    sharp_weights(r, ri, p.inv_delta[0], tab, A1, A3, A5);
+    if (MODE & 1) {
+      const double alpha = tf[NF_ALPHA][lane];
+      const double gx = fma(-alpha, s.mx, s.fx), gy = fma(-alpha, s.my, s.fy), gz = fma(-alpha, s.mz, s.fz);
+      const double dg = fma(dx, gx, fma(dy, gy, dz * gz)) * A3;
+      a.u0 = fma(gx, A1, dx * dg);
+      a.u1 = fma(gy, A1, dy * dg);
+      a.u2 = fma(gz, A1, dz * dg);
+    }
+    if (MODE & 2) {
+      const double qx = s.qx - tf[NF_Q0][lane], qy = s.qy - tf[NF_Q1][lane], qz = s.qz - tf[NF_Q2][lane];
+      const double c = fma(dx, qx, fma(dy, qy, dz * qz)) * fma(dx, s.mx, fma(dy, s.my, dz * s.mz)) * A5;
+      a.v0 = dx * c;
+      a.v1 = dy * c;
+      a.v2 = dz * c;
+    }
+    return a;
+  }
   // all three deltas through the branch-free table path (independent chains)
   const double t0 = r * p.inv_delta[0], t1 = r * p.inv_delta[1], t2 = r * p.inv_delta[2];
   double E0, E1, E2, s20, s21, s22, c0, c1, c2;
@@ -567,7 +587,7 @@ constexpr int kQCap = 64;  // per-lane ring capacity (power of two)
 #ifndef SER_NEAR_MINB
 #define SER_NEAR_MINB 4
 #endif
-template <int MODE>
+template <int MODE, bool SHARP>
 __global__ void __launch_bounds__(kNearWarps * 32, SER_NEAR_MINB) near_kernel(const NearParams p) {
   __shared__ double s_tab[kErfcxPieces * kErfcxStride];
   __shared__ double s_sx[kNearWarps][3][32];
@@ -683,7 +703,7 @@ __global__ void __launch_bounds__(kNearWarps * 32, SER_NEAR_MINB) near_kernel(co
           const int sidx = q[head & (kQCap - 1)][lane];
           ++head;
           const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
-          const Acc d = near_pair<MODE>(s, y0, y1, y2, tf, lane, p, s_tab);
+          const Acc d = near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, s_tab);
           acc.u0 += d.u0; acc.u1 += d.u1; acc.u2 += d.u2;
           acc.v0 += d.v0; acc.v1 += d.v1; acc.v2 += d.v2;
         }

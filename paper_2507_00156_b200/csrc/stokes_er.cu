@@ -199,10 +199,10 @@ bool rho_ok(const double* rho) {
 
 int validate(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
              const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
-             const double* rho, int mode) {
+             const double* rho, int mode, bool check_rho = true) {
   if (mode < 1 || mode > 3) return STOKES_ER_EINVAL;
   if (M < 0 || N < 1 || M > INT32_MAX || N > INT32_MAX) return STOKES_ER_EINVAL;
-  if (!(h > 0.0) || !std::isfinite(h) || !rho_ok(rho)) return STOKES_ER_EINVAL;
+  if (!(h > 0.0) || !std::isfinite(h) || (check_rho && !rho_ok(rho))) return STOKES_ER_EINVAL;
   if (!sx || !sn || !sw) return STOKES_ER_EINVAL;
   if (M > 0 && (!ty || !tb || !x0d)) return STOKES_ER_EINVAL;  // M == 0: no target arrays needed
   if ((mode & 1) && !f) return STOKES_ER_EINVAL;
@@ -229,7 +229,9 @@ void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
   far_kernel<MODE, T><<<grid, kThreads, 0, s>>>(pp);
 }
 
-template <int MODE>
+// SHARP = NEXT-1 on-surface variant: h = delta, rho = (1,1,1), weights (1,0,0),
+// cutoff STOKES_ER_CUTOFF_SURFACE; otherwise the 3-delta extrapolated method.
+template <int MODE, bool SHARP>
 int run_eval(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
              const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
              const double* rho, double* out_u, double* out_v, char* ws, const Plan& P, cudaStream_t s,
@@ -264,7 +266,8 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
     return STOKES_ER_ECUDA;
   pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox);
   Delta3 r3{{rho[0], rho[1], rho[2]}};
-  pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, tgt, orig);
+  pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt,
+                                                            orig);
   if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
 
   PairParams pp;
@@ -279,7 +282,8 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   pp.chunk_tiles = P.chunk_tiles;
   pp.n_tiles = P.n_tiles;
   const double dmax = rho[2] * h;
-  pp.rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  const double cutoff = SHARP ? STOKES_ER_CUTOFF_SURFACE : STOKES_ER_CUTOFF;
+  pp.rc2 = (cutoff * dmax) * (cutoff * dmax);
   pp.rc2_box = pp.rc2 * (1.0 + 1e-9);
   pp.r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
   for (int k = 0; k < 3; ++k) pp.inv_delta[k] = 1.0 / (rho[k] * h);
@@ -313,10 +317,10 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_kernel<MODE>, kNearWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_kernel<MODE, SHARP>, kNearWarps * 32, 0);
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(occ, 1))));
-    near_kernel<MODE><<<grid, kNearWarps * 32, 0, s>>>(np);
+    near_kernel<MODE, SHARP><<<grid, kNearWarps * 32, 0, s>>>(np);
   }
   if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
   if (opt) {
@@ -358,12 +362,13 @@ size_t stokes_er_workspace_bytes_ex(int64_t M, int64_t N, int mode, const stokes
                   make_plan(M, N, mode, opt_T(options), opt_chunk(options), opt_phases(options)).total);
 }
 
-int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const double* src_weight,
-                      const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
-                      const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
-                      int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
-                      void* stream, stokes_er_options* options) {
-  int st = validate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode);
+static int eval_common(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
+                       const double* q, const double* tgt_xyz, const double* tgt_b, const double* tgt_x0_density,
+                       int64_t M, int64_t N, double h, const double rho[3], int mode, double* out_u,
+                       double* out_v, void* workspace, size_t workspace_bytes, void* stream,
+                       stokes_er_options* options, bool sharp) {
+  int st = validate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode,
+                    !sharp);
   if (st) return st;
   if (M == 0) return STOKES_ER_OK;
   if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
@@ -372,17 +377,41 @@ int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const dou
   if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(workspace);
-  switch (mode) {
-    case 1:
-      return run_eval<1>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho,
-                         out_u, out_v, ws, P, s, options);
-    case 2:
-      return run_eval<2>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho,
-                         out_u, out_v, ws, P, s, options);
-    default:
-      return run_eval<3>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho,
-                         out_u, out_v, ws, P, s, options);
+#define SER_RUN(M_, S_)                                                                                          \
+  run_eval<M_, S_>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, out_u, \
+                   out_v, ws, P, s, options)
+  if (sharp) {
+    switch (mode) {
+      case 1: return SER_RUN(1, true);
+      case 2: return SER_RUN(2, true);
+      default: return SER_RUN(3, true);
+    }
   }
+  switch (mode) {
+    case 1: return SER_RUN(1, false);
+    case 2: return SER_RUN(2, false);
+    default: return SER_RUN(3, false);
+  }
+#undef SER_RUN
+}
+
+int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const double* src_weight,
+                      const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                      const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
+                      int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
+                      void* stream, stokes_er_options* options) {
+  return eval_common(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode,
+                     out_u, out_v, workspace, workspace_bytes, stream, options, false);
+}
+
+int stokes_er_eval_onsurface(const double* src_xyz, const double* src_normal, const double* src_weight,
+                             const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                             const double* tgt_x0_density, int64_t M, int64_t N, double delta, int mode,
+                             double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  const double one[3] = {1.0, 1.0, 1.0};  // delta_1 = delta_2 = delta_3 = delta; weights (1, 0, 0)
+  return eval_common(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, delta, one, mode,
+                     out_u, out_v, workspace, workspace_bytes, stream, nullptr, true);
 }
 
 int stokes_er_eval(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,

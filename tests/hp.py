@@ -110,3 +110,62 @@ def brute_deltas(block, targets, mode=3):
                 out[k][0][i][ti] = U[k][i] / (8 * mp.pi)
                 out[k][1][i][ti] = V[k][i] / (8 * mp.pi) + chi * q0[i]
     return out
+
+
+def brute_sharp(block, targets, delta, cutoff=None):
+    """NEXT-1 on-surface variant at 50 digits: S^d with s1#, s2# (eq. 12 with the
+    s# of PAPER.md:130-138) and the unsplit stresslet times s3# (R16).
+    `cutoff` (in units of delta) applies s# = 1 beyond it, as the localized oracle does.
+    Returns (u list[3][T], v list[3][T])."""
+    N = block.N
+    d = mp.mpf(delta)
+    U = [[None] * len(targets) for _ in range(3)]
+    V = [[None] * len(targets) for _ in range(3)]
+    for ti, t in enumerate(targets):
+        y = [mp.mpf(float(block.tgt_xyz[i, t])) for i in range(3)]
+        b = mp.mpf(float(block.tgt_b[t]))
+        n0 = [mp.mpf(float(block.tgt_x0_density[i, t])) for i in range(3)]
+        f0 = [mp.mpf(float(block.tgt_x0_density[3 + i, t])) for i in range(3)]
+        q0 = [mp.mpf(float(block.tgt_x0_density[6 + i, t])) for i in range(3)]
+        alpha = sum(f0[i] * n0[i] for i in range(3))
+        chi = mp.mpf(1) if b < 0 else (mp.mpf(0) if b > 0 else mp.mpf(1) / 2)
+        u = [mp.mpf(0)] * 3
+        v = [mp.mpf(0)] * 3
+        for s in range(N):
+            x = [mp.mpf(float(block.src_xyz[i, s])) for i in range(3)]
+            m = [mp.mpf(float(block.src_normal[i, s])) for i in range(3)]
+            w = mp.mpf(float(block.src_weight[s]))
+            yh = [y[i] - x[i] for i in range(3)]
+            r = mp.sqrt(sum(c * c for c in yh))
+            g = [mp.mpf(float(block.f[a, s])) - alpha * m[a] for a in range(3)]
+            dq = [mp.mpf(float(block.q[a, s])) - q0[a] for a in range(3)]
+            if r == 0:
+                A1, A3, A5 = (lim / d ** p for lim, p in zip(sharp_limits(), (1, 3, 5)))
+            else:
+                s1, s2, s3 = s_sharp(r / d) if (cutoff is None or r / d <= cutoff) else (1, 1, 1)
+                A1, A3, A5 = s1 / r, s2 / r ** 3, s3 / r ** 5
+            yg = sum(yh[a] * g[a] for a in range(3))
+            yq = sum(yh[a] * dq[a] for a in range(3))
+            ym = sum(yh[c] * m[c] for c in range(3))
+            for i in range(3):
+                u[i] += w * (g[i] * A1 + yh[i] * yg * A3)
+                v[i] += w * (-6) * yh[i] * yq * ym * A5
+        for i in range(3):
+            U[i][ti] = u[i] / (8 * mp.pi)
+            V[i][ti] = v[i] / (8 * mp.pi) + chi * q0[i]
+    return U, V
+
+
+def sharp_limits():
+    """lim_{t->0} s#_i(t)/t^p for p = 1, 3, 5, evaluated numerically at t = 1e-40 with
+    400 digits (independent of the series the oracle's comments derive)."""
+    with mp.workdps(400):
+        t = mp.mpf(10) ** -40
+        sq = mp.sqrt(mp.pi)
+        E = mp.erf(t)
+        e = mp.exp(-t * t)
+        s1 = E + 2 / (3 * sq) * (5 * t - 2 * t ** 3) * e
+        s2 = E - 2 / (3 * sq) * (3 * t - 14 * t ** 3 + 4 * t ** 5) * e
+        s3 = E - 2 / (9 * sq) * (9 * t + 6 * t ** 3 - 4 * t ** 5) * e
+        out = (s1 / t, s2 / t ** 3, s3 / t ** 5)
+    return tuple(mp.mpf(x) for x in out)

@@ -218,3 +218,36 @@ def test_far_targets_pass_through(ser):
     blk = pure_far(inv_h=32, b=0.9)
     blk = blk.take_targets(np.arange(0, blk.M, 11))
     check_block(ser, blk, localized=False)
+
+
+# ---------------------------------------------------------------- NEXT-1
+def _onsurface(ser, block, delta, mode=3):
+    arrs = ser.to_device(block)
+    u, v = ser.evaluate_onsurface(*arrs, delta, mode=mode)
+    return (None if u is None else u.cpu().numpy()), (None if v is None else v.cpu().numpy())
+
+
+@pytest.mark.parametrize("inv_h", [16, 32])
+def test_onsurface_sharp_parity(ser, inv_h):
+    """stokes_er_eval_onsurface (s#, delta = 3h) vs the oracle's
+    sharp mode (definition: every pair regularized) on all sphere nodes."""
+    blk = config5(inv_h=inv_h)
+    if inv_h == 32:
+        blk = blk.take_targets(np.arange(0, blk.M, 7))
+    delta = 3 * blk.h
+    u, v = _onsurface(ser, blk, delta)
+    ur, vr = oracle.evaluate_sharp(*blk.arrays(), delta, localized=False, cutoff=7.0)
+    assert rel(u, ur) <= TOL and rel(v, vr) <= TOL
+
+
+def test_onsurface_two_sphere_self_block(ser):
+    blk = config4(eps=0.05, inv_h=32)[0]
+    blk = blk.take_targets(np.arange(0, blk.M, 5))
+    delta = 3 * blk.h
+    for mode in (1, 2, 3):
+        u, v = _onsurface(ser, blk, delta, mode=mode)
+        ur, vr = oracle.evaluate_sharp(*blk.arrays(), delta, mode=mode, localized=True, cutoff=7.0)
+        if mode & 1:
+            assert rel(u, ur) <= TOL
+        if mode & 2:
+            assert rel(v, vr) <= TOL

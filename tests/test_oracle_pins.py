@@ -268,3 +268,59 @@ def test_invalid_arguments(oracle_mod):
         oracle_mod.evaluate(*blk.arrays(), -1.0, blk.rho)
     with pytest.raises(ValueError):
         oracle_mod.evaluate(*blk.arrays(), blk.h, (3.0, 3.0, 4.0))
+
+
+# ------------------------------------------------- NEXT-1: on-surface s# variant
+def _surface_block(inv_h, f_field, q_field, k=60, seed=0):
+    from workloads.configs import make_block
+    from workloads.quadrature import quadrature, sphere
+    h = 1.0 / inv_h
+    x, n, w, _ = quadrature(sphere(), h)
+    pick = np.random.default_rng(seed).choice(x.shape[1], k, replace=False)
+    return make_block(sphere(), h, x[:, pick], np.zeros(k), x[:, pick], n[:, pick], f_field, q_field, src=(x, n, w))
+
+
+def test_sharp_on_surface_closed_forms_converge(oracle_mod):
+    """PAPER.md:126-139: s# gives O(delta^5) on the surface without extrapolation
+    (delta = 3h).  SL translation/rotation and Green's identity
+    (shear flow, chi = 1/2) against closed forms; error ratio 1/16 -> 1/32 > 2^4."""
+    errs = {}
+    for inv in (16, 32):
+        h = 1.0 / inv
+        e = {}
+        blk = _surface_block(inv, ConstField(F_T), ConstField(Q_C))
+        u, v = oracle_mod.evaluate_sharp(*blk.arrays(), 3 * h, localized=True, cutoff=7.0)
+        e["sl_transl"] = np.abs(u - sl_translation(F_T, blk.tgt_xyz)).max()
+        assert np.abs(v - 0.5 * Q_C[:, None]).max() < 1e-14
+        blk = _surface_block(inv, RigidField(Omega=OMEGA), RigidField(**RIGID))
+        u, v = oracle_mod.evaluate_sharp(*blk.arrays(), 3 * h, localized=True, cutoff=7.0)
+        e["sl_rot"] = np.abs(u - sl_rotation(OMEGA, blk.tgt_xyz)).max()
+        blk = _surface_block(inv, LinearField(SHEAR_TRACTION), LinearField(SHEAR_VELOCITY))
+        u, v = oracle_mod.evaluate_sharp(*blk.arrays(), 3 * h, localized=True, cutoff=7.0)
+        e["green"] = np.abs(u + v - 0.5 * (SHEAR_VELOCITY @ blk.tgt_xyz)).max()
+        errs[inv] = e
+    for k in errs[16]:
+        assert errs[32][k] < 5e-7, (k, errs[32][k])
+        assert errs[16][k] / errs[32][k] > 16, (k, errs[16][k], errs[32][k])
+
+
+def test_sharp_brute_force_mpmath(oracle_mod):
+    """oracle_eval_sharp (definition mode, no cutoff) vs the 50-digit brute force,
+    including coincident-node targets (r = 0 limits of s#/t^p)."""
+    from workloads.densities import PolyField
+    rng = np.random.default_rng(21)
+    blk = _surface_block(4, PolyField(rng), PolyField(rng), k=4, seed=3)
+    delta = 3 * blk.h
+    U, V = hp.brute_sharp(blk, list(range(blk.M)), delta)
+    u, v = oracle_mod.evaluate_sharp(*blk.arrays(), delta, localized=False, cutoff=7.0)
+    ur = np.array([[float(a) for a in row] for row in U])
+    vr = np.array([[float(a) for a in row] for row in V])
+    assert np.abs(u - ur).max() <= 1e-14 * np.abs(ur).max()
+    assert np.abs(v - vr).max() <= 1e-14 * np.abs(vr).max()
+
+
+def test_sharp_cutoff_seven(oracle_mod):
+    """Reading R15: 1 - s2#(6) = 2.45e-12 is not negligible, 1 - s_i#(7) < 1e-16."""
+    assert abs(1 - float(hp.s_sharp(6.0)[1])) == pytest.approx(2.45e-12, rel=0.01)
+    for v in hp.s_sharp(7.0):
+        assert abs(1 - float(v)) < 1e-16
