@@ -328,6 +328,42 @@ __device__ __forceinline__ void far_pair(const Src& s, const Tgt& t, Acc& a) {
   }
 }
 
+// far_pair split in two halves for software pipelining (K1's all-far loop):
+// far_geo (d, r^2 and the MUFU + Newton rsqrt: the long dependency chain) of
+// source k+1 is issued before far_acc (the SL/DL contractions) of source k.
+struct Geo {
+  double dx, dy, dz, ri;
+};
+__device__ __forceinline__ Geo far_geo(const Src& s, const Tgt& t) {
+  Geo g;
+  g.dx = t.y0 - s.x;
+  g.dy = t.y1 - s.y;
+  g.dz = t.y2 - s.z;
+  g.ri = rsqrt_nr(fma(g.dx, g.dx, fma(g.dy, g.dy, g.dz * g.dz)));
+  return g;
+}
+template <int MODE>
+__device__ __forceinline__ void far_acc(const Src& s, const Tgt& t, const Geo& g, Acc& a) {
+  const double dx = g.dx, dy = g.dy, dz = g.dz, ri = g.ri;
+  const double ri2 = ri * ri;
+  if (MODE & 1) {
+    const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
+    const double a3 = fma(dx, gx, fma(dy, gy, dz * gz)) * ri2;
+    a.u0 = fma(fma(dx, a3, gx), ri, a.u0);
+    a.u1 = fma(fma(dy, a3, gy), ri, a.u1);
+    a.u2 = fma(fma(dz, a3, gz), ri, a.u2);
+  }
+  if (MODE & 2) {
+    const double qx = s.qx - t.q0, qy = s.qy - t.q1, qz = s.qz - t.q2;
+    const double dq = fma(dx, qx, fma(dy, qy, dz * qz));
+    const double dm = fma(dx, s.mx, fma(dy, s.my, dz * s.mz));
+    const double c = (dq * dm) * (ri2 * ri2 * ri);
+    a.v0 = fma(dx, c, a.v0);
+    a.v1 = fma(dy, c, a.v1);
+    a.v2 = fma(dz, c, a.v2);
+  }
+}
+
 // Far pair with the near pairs of a mixed sub-tile masked out: ri := 0 zeroes
 // every term of far_pair (u += (g + d a3) 0, c = .. ri^5 = 0) at the cost of
 // one compare and a select; the near kernel owns those pairs.
@@ -439,11 +475,23 @@ __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) far_kernel(const PairP
         }
         const double* ss = sm + sub * kSub * kSrcDoubles;
         if (g2 > p.rc2_box) {  // warp-uniform: every pair of this sub-tile is far
+          // software pipeline: geometry + rsqrt of source k+1 overlap the
+          // contractions of source k (the last step recomputes source 0: discarded)
+          Src s = load_src<MODE>(ss);
+          Geo g[T];
+#pragma unroll
+          for (int j = 0; j < T; ++j) g[j] = far_geo(s, tg[j]);
 #pragma unroll kFarUnroll
           for (int k = 0; k < kSub; ++k) {
-            const Src s = load_src<MODE>(ss + k * kSrcDoubles);
+            const Src sn = load_src<MODE>(ss + ((k + 1) & (kSub - 1)) * kSrcDoubles);
+            Geo gn[T];
 #pragma unroll
-            for (int j = 0; j < T; ++j) far_pair<MODE>(s, tg[j], acc[j]);
+            for (int j = 0; j < T; ++j) gn[j] = far_geo(sn, tg[j]);
+#pragma unroll
+            for (int j = 0; j < T; ++j) far_acc<MODE>(s, tg[j], g[j], acc[j]);
+            s = sn;
+#pragma unroll
+            for (int j = 0; j < T; ++j) g[j] = gn[j];
           }
         } else {  // mixed: far pairs only, near pairs belong to the near kernel
 #pragma unroll 2
