@@ -637,13 +637,10 @@ constexpr int kQCap = 64;  // per-lane ring capacity (power of two)
 #endif
 template <int MODE, bool SHARP>
 __global__ void __launch_bounds__(kNearWarps * 32, SER_NEAR_MINB) near_kernel(const NearParams p) {
-  __shared__ double s_tab[kErfcxPieces * kErfcxStride];
   __shared__ double s_sx[kNearWarps][3][32];
   __shared__ int s_q[kNearWarps][kQCap][32];
   __shared__ double s_tf[kNearWarps][kNearFields][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kErfcxPieces * kErfcxStride; i += blockDim.x) s_tab[i] = kErfcxTable[i];
-  __syncthreads();
   int(*q)[32] = s_q[warp];
   double(*tf)[32] = s_tf[warp];
   const int n_sub = static_cast<int>(p.Npad / kSub);
@@ -751,7 +748,7 @@ __global__ void __launch_bounds__(kNearWarps * 32, SER_NEAR_MINB) near_kernel(co
           const int sidx = q[head & (kQCap - 1)][lane];
           ++head;
           const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
-          const Acc d = near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, s_tab);
+          const Acc d = near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, nullptr);
           acc.u0 += d.u0; acc.u1 += d.u1; acc.u2 += d.u2;
           acc.v0 += d.v0; acc.v1 += d.v1; acc.v2 += d.v2;
         }
