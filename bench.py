@@ -39,6 +39,7 @@ UNIT = "pairs/s"
 F_FAR_ALG = 57
 F_NEAR_ALG = 180
 F_FAR_ISSUED = 64   # ncu-countable FP64 flops (2*DFMA + DMUL + DADD) of far_pair<3> (41 instructions)
+F_NEAR_ISSUED = 378  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r01/ncu_full_v8: 144 DFMA, 60 DMUL, 30 DADD)
 SMS = 148
 FP64_LANES_PER_SM = 64  # measured: DFMA loop 58.7 FMA/clk/SM at the boost clock (tools/probes)
 
@@ -55,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
     ap.add_argument("--near-phases", type=int, default=0)
+    ap.add_argument("--schedule", choices=["fused", "separate"], default="fused",
+                    help="fused: one persistent kernel, far items and near items from one interleaved "
+                         "queue (default); separate: far kernel then near kernel")
     return ap.parse_args()
 
 
@@ -227,6 +231,8 @@ def main():
         opt.targets_per_thread = args.targets_per_thread
     if args.near_phases:
         opt.near_phases = args.near_phases
+    fused = args.schedule != "separate"
+    opt.schedule = {"fused": 0, "separate": 1}[args.schedule]
     nbytes = int(ser._lib.load().stokes_er_workspace_bytes_ex(M, N, 3, __import__("ctypes").byref(opt)))
     ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -306,27 +312,41 @@ def main():
 
     clocks = clk.summary()
     far_avg_s = statistics.mean(pair_ms) / 1e3
-    near_avg_s = statistics.mean(near_ms) / 1e3
     far = pairs - near
     f_clk = 1965.0
     peak = SMS * FP64_LANES_PER_SM * 2 * f_clk * 1e6 / 1e12  # TFLOP/s
-    far_flops = far * F_FAR_ALG
-    achieved = far_flops / far_avg_s / 1e12
+    peak_source = "derived: 148 SMs x 64 FP64 FMA/clk/SM (DFMA-loop probe) x 2 x 1965 MHz max SM clock"
+    if fused:
+        # the dominant (and only pair) kernel does the far AND the near pairs
+        k_flops = far * F_FAR_ALG + near * F_NEAR_ALG
+        k_issued = far * F_FAR_ISSUED + near * F_NEAR_ISSUED
+        kname = ("fused_kernel<3,T> (FP64 pipe): far-field sum (PAPER.md:183-191) + near 3-delta sums "
+                 "with the folded extrapolation (PAPER.md:82-123), one persistent kernel")
+        conv = (f"{F_FAR_ALG} algorithmic flops per far pair + {F_NEAR_ALG} per near pair "
+                "(rsqrt/erf/exp = 1, FMA = 2)")
+    else:
+        k_flops = far * F_FAR_ALG
+        k_issued = far * F_FAR_ISSUED
+        kname = "far_kernel<3,T> (FP64 pipe): the shared far-field sum, PAPER.md:183-191"
+        conv = f"{F_FAR_ALG} algorithmic flops per far pair (rsqrt = 1, FMA = 2)"
+    achieved = k_flops / far_avg_s / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None,
-                "kernel": "far_kernel<3,T> (FP64 pipe): the shared far-field sum, PAPER.md:183-191",
-                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM (DFMA-loop probe) x 2 x 1965 MHz max SM clock",
-                "flops_per_launch": far_flops, "flop_convention": f"{F_FAR_ALG} algorithmic flops per far pair "
-                                                                   "(rsqrt = 1, FMA = 2)",
-                "frac_issued_convention": far * F_FAR_ISSUED / far_avg_s / 1e12 / peak,
-                "far_kernel_ms": far_avg_s * 1e3,
-                "far_kernel_share": sum(pair_ms) / sum(step_ms),
-                "far_pairs_per_s": far / far_avg_s}
+                "traffic": None, "kernel": kname, "peak_source": peak_source,
+                "flops_per_launch": k_flops, "flop_convention": conv,
+                "frac_issued_convention": k_issued / far_avg_s / 1e12 / peak,
+                "kernel_ms": far_avg_s * 1e3,
+                "kernel_share": sum(pair_ms) / sum(step_ms),
+                "far_pairs": far, "near_pairs": near}
     if clocks.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (SMS * FP64_LANES_PER_SM * 2 * clocks["sm_mhz"] / 1e6)
-    near_info = {"kernel": "near_kernel<3>", "ms": near_avg_s * 1e3, "share": sum(near_ms) / sum(step_ms),
-                 "near_pairs": near, "near_pairs_per_s": near / near_avg_s,
-                 "tflops_alg": near * F_NEAR_ALG / near_avg_s / 1e12}
+    if fused:
+        near_info = None
+    else:
+        near_avg_s = statistics.mean(near_ms) / 1e3
+        roofline["far_pairs_per_s"] = far / far_avg_s
+        near_info = {"kernel": "near_kernel<3>", "ms": near_avg_s * 1e3, "share": sum(near_ms) / sum(step_ms),
+                     "near_pairs": near, "near_pairs_per_s": near / near_avg_s,
+                     "tflops_alg": near * F_NEAR_ALG / near_avg_s / 1e12}
     alg_flops = far * F_FAR_ALG + near * F_NEAR_ALG
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -336,13 +356,17 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM",
                        "targets_per_thread": int(opt.stats[3]), "work_items": int(opt.stats[0]),
                        "grid_ctas": int(opt.stats[1]), "chunk_tiles": int(opt.stats[2]),
+                       "schedule": args.schedule,
                        "parallelism": f"target-sharded x{world} (independent instances)"},
             "fp64_tflops_alg": alg_flops * K * world / total_s / 1e12,
-            "roofline": roofline, "near_kernel": near_info, "clocks": clocks,
-            "gpu_launches": K * ser.launch_count(M, N, 3),
-            "gpu_launches_note": "our kernels per step: bbox, 2 morton, pack_sources, pack_targets, far, near, finalize "
+            "roofline": roofline, "clocks": clocks,
+            "gpu_launches": K * (ser.launch_count(M, N, 3) + (0 if fused else 1)),
+            "gpu_launches_note": "our kernels per step: bbox, 2 morton, pack_sources, pack_targets, "
+                                 + ("fused far+near" if fused else "far, near") + ", finalize "
                                  "(+ CUB radix-sort launches, library code)",
             "e2e": e2e}
+    if near_info is not None:
+        line["near_kernel"] = near_info
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(block)
     print(json.dumps(line), flush=True)

@@ -167,7 +167,18 @@ typedef struct {
   void* near_kernel_start_event; /* optional events around the near-field kernel */
   void* near_kernel_end_event;
   int near_phases;               /* 0 = automatic; near work units per 32-target group (1..64) */
+  int schedule;                  /* STOKES_ER_SCHEDULE_FUSED (0, default): one persistent kernel whose
+                                    CTAs take far items (a target block x a source chunk) and near
+                                    items (one near unit per warp) from one queue that interleaves
+                                    them, so far and near work share every SM's FP64 pipe;
+                                    STOKES_ER_SCHEDULE_SEPARATE (1): far kernel, then near kernel.
+                                    Both give the same sums (same per-slot partials, same fixed-order
+                                    finalize).  FUSED records only the pair_kernel events (around
+                                    the one pair kernel). */
 } stokes_er_options;
+
+#define STOKES_ER_SCHEDULE_FUSED 0
+#define STOKES_ER_SCHEDULE_SEPARATE 1
 
 /* Workspace for stokes_er_eval_ex with these tuning options (>= stokes_er_workspace_bytes
  * when the options force a finer source chunking). */

@@ -27,7 +27,8 @@ class Options(ctypes.Structure):
     _fields_ = [("pair_kernel_start_event", ctypes.c_void_p), ("pair_kernel_end_event", ctypes.c_void_p),
                 ("targets_per_thread", ctypes.c_int), ("source_chunk_tiles", ctypes.c_int),
                 ("stats", ctypes.c_int64 * 4), ("near_kernel_start_event", ctypes.c_void_p),
-                ("near_kernel_end_event", ctypes.c_void_p), ("near_phases", ctypes.c_int)]
+                ("near_kernel_end_event", ctypes.c_void_p), ("near_phases", ctypes.c_int),
+                ("schedule", ctypes.c_int)]
 
 
 EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_er_eval", "stokes_er_eval_ex", "stokes_er_host_workspace_bytes",

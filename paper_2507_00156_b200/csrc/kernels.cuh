@@ -63,6 +63,7 @@ struct PairParams {
   int n_items, n_chunks, chunk_tiles, n_tiles;
   double rc2;             // (c delta_max)^2: near iff r^2 <= rc2
   double rc2_box;         // conservative bound for sub-tile tests
+  double rc2_inner;       // sub-tiles whose farthest pair is within this are all-near (skipped)
   double r2_tiny;         // (1e-8 delta_1)^2: r -> 0 limits below (R3)
   double inv_delta[3];
 };
@@ -112,6 +113,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+
+// Barrier of the kThreads far-item threads (warps 0 .. kThreads/32 - 1): named
+// barrier 1, so a warp-specialized CTA's near warps never take part.
+__device__ __forceinline__ void far_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(SER_FAR_THREADS) : "memory"); }
 
 // ------------------------------------------------------------ K0: pack & sort
 __device__ __forceinline__ uint32_t spread10(uint32_t v) {
@@ -391,10 +396,122 @@ __device__ __forceinline__ void far_pair_masked(const Src& s, const Tgt& t, Acc&
   }
 }
 
-// K1: far-field pair sums (the non-local part, computed once
-// and shared by the three deltas).  Persistent CTAs pull (target block,
-// source chunk) items from a queue; each item's partial sums go to their own
-// slot, summed in fixed order by the finalize (deterministic).
+// K1 body: one far work item = (target block of kThreads*T targets, source
+// chunk) -- the far-field pair sums (the non-local part,
+// computed once and shared by the three deltas).  Each item's partial sums go
+// to their own slot, summed in fixed order by the finalize (deterministic).
+// Source tiles are TMA bulk copies into the double buffer `tile` (completion on
+// bar[0..1]; parities carried across items by the caller).
+template <int MODE, int T>
+__device__ __forceinline__ void far_item(const PairParams& p, int item, double (*tile)[kTile * kSrcDoubles],
+                                         uint64_t* bar, uint32_t& parity0, uint32_t& parity1) {
+  constexpr int TB = kThreads * T;  // targets per block
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tb = item / p.n_chunks, ch = item - tb * p.n_chunks;
+  const int tile0 = ch * p.chunk_tiles;
+  const int ntiles = min(p.chunk_tiles, p.n_tiles - tile0);
+  const double* src_base = p.src + (int64_t)tile0 * kTile * kSrcDoubles;
+  if (tid == 0) {  // prefetch the first tile of this item
+    // order the CTA's earlier generic-proxy SMEM accesses (the fused kernel's
+    // near units alias this buffer; the caller's far-group barrier precedes) before
+    // the async-proxy (TMA) writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[0], kTileBytes);
+    bulk_g2s(tile[0], src_base, kTileBytes, &bar[0]);
+  }
+
+  // targets of this thread: warp-contiguous (Morton order) -> tight warp boxes
+  Tgt tg[T];
+  Acc acc[T];
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+#pragma unroll
+  for (int j = 0; j < T; ++j) {
+    const int64_t i = (int64_t)tb * TB + warp * 32 * T + j * 32 + lane;
+    const double* q = p.tgt + i;
+    tg[j].y0 = q[F_Y0 * p.Mpad];
+    tg[j].y1 = q[F_Y1 * p.Mpad];
+    tg[j].y2 = q[F_Y2 * p.Mpad];
+    tg[j].alpha = (MODE & 1) ? q[F_ALPHA * p.Mpad] : 0.0;
+    tg[j].q0 = (MODE & 2) ? q[F_Q0 * p.Mpad] : 0.0;
+    tg[j].q1 = (MODE & 2) ? q[F_Q1 * p.Mpad] : 0.0;
+    tg[j].q2 = (MODE & 2) ? q[F_Q2 * p.Mpad] : 0.0;
+    acc[j] = Acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    lo[0] = fmin(lo[0], tg[j].y0); hi[0] = fmax(hi[0], tg[j].y0);
+    lo[1] = fmin(lo[1], tg[j].y1); hi[1] = fmax(hi[1], tg[j].y1);
+    lo[2] = fmin(lo[2], tg[j].y2); hi[2] = fmax(hi[2], tg[j].y2);
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    for (int o = 16; o; o >>= 1) {
+      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int buf = t & 1;
+    if (tid == 0 && t + 1 < ntiles) {  // the other buffer was released by the far_bar_sync below
+      mbar_expect_tx(&bar[buf ^ 1], kTileBytes);
+      bulk_g2s(tile[buf ^ 1], src_base + (int64_t)(t + 1) * kTile * kSrcDoubles, kTileBytes, &bar[buf ^ 1]);
+    }
+    if (buf == 0) { mbar_wait(&bar[0], parity0); parity0 ^= 1; }
+    else { mbar_wait(&bar[1], parity1); parity1 ^= 1; }
+    const double* sm = tile[buf];
+    const double* boxes = p.src_box + ((int64_t)(tile0 + t) * (kTile / kSub)) * 8;
+#pragma unroll 1
+    for (int sub = 0; sub < kTile / kSub; ++sub) {
+      const double* bx = boxes + sub * 8;
+      double g2 = 0.0, f2 = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double blo = __ldg(bx + d), bhi = __ldg(bx + 4 + d);
+        const double gap = fmax(0.0, fmax(blo - hi[d], lo[d] - bhi));
+        const double span = fmax(bhi - lo[d], hi[d] - blo);  // largest coordinate distance
+        g2 = fma(gap, gap, g2);
+        f2 = fma(span, span, f2);
+      }
+      const double* ss = sm + sub * kSub * kSrcDoubles;
+      if (g2 > p.rc2_box) {  // warp-uniform: every pair of this sub-tile is far
+        // software pipeline: geometry + rsqrt of source k+1 overlap the
+        // contractions of source k (the last step recomputes source 0: discarded)
+        Src s = load_src<MODE>(ss);
+        Geo g[T];
+#pragma unroll
+        for (int j = 0; j < T; ++j) g[j] = far_geo(s, tg[j]);
+#pragma unroll kFarUnroll
+        for (int k = 0; k < kSub; ++k) {
+          const Src sn = load_src<MODE>(ss + ((k + 1) & (kSub - 1)) * kSrcDoubles);
+          Geo gn[T];
+#pragma unroll
+          for (int j = 0; j < T; ++j) gn[j] = far_geo(sn, tg[j]);
+#pragma unroll
+          for (int j = 0; j < T; ++j) far_acc<MODE>(s, tg[j], g[j], acc[j]);
+          s = sn;
+#pragma unroll
+          for (int j = 0; j < T; ++j) g[j] = gn[j];
+        }
+      } else if (f2 > p.rc2_inner) {  // mixed: far pairs only, near pairs belong to the near kernel
+#pragma unroll 2
+        for (int k = 0; k < kSub; ++k) {
+          const Src s = load_src<MODE>(ss + k * kSrcDoubles);
+#pragma unroll
+          for (int j = 0; j < T; ++j) far_pair_masked<MODE>(s, tg[j], acc[j], p.rc2);
+        }
+      }  // else: every pair of the sub-tile is near (r^2 <= rc2): nothing far to add
+    }
+    far_bar_sync();  // all reads of `buf` done before it is refilled
+  }
+
+  // partial sums of this item: [item][6][TB]
+  double* out = p.partial + (int64_t)item * 6 * TB;
+#pragma unroll
+  for (int j = 0; j < T; ++j) {
+    const int loc = warp * 32 * T + j * 32 + lane;
+    if (MODE & 1) { out[0 * TB + loc] = acc[j].u0; out[1 * TB + loc] = acc[j].u1; out[2 * TB + loc] = acc[j].u2; }
+    if (MODE & 2) { out[3 * TB + loc] = acc[j].v0; out[4 * TB + loc] = acc[j].v1; out[5 * TB + loc] = acc[j].v2; }
+  }
+}
+
+// K1 (separate schedule): persistent CTAs pull far items from a queue.
 template <int MODE, int T>
 #ifndef SER_FAR_MINB
 #define SER_FAR_MINB (512 / SER_FAR_THREADS)
@@ -403,116 +520,20 @@ __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) far_kernel(const PairP
   __shared__ __align__(128) double tile[2][kTile * kSrcDoubles];
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int s_item;
-  constexpr int TB = kThreads * T;  // targets per block
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
   uint32_t parity0 = 0, parity1 = 0;
-
   for (;;) {
-    if (tid == 0) s_item = atomicAdd(p.counter, 1);
+    if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1);
     __syncthreads();
     const int item = s_item;
+    __syncthreads();  // every thread has read s_item before thread 0 may overwrite it
     if (item >= p.n_items) break;
-    const int tb = item / p.n_chunks, ch = item - tb * p.n_chunks;
-    const int tile0 = ch * p.chunk_tiles;
-    const int ntiles = min(p.chunk_tiles, p.n_tiles - tile0);
-    const double* src_base = p.src + (int64_t)tile0 * kTile * kSrcDoubles;
-    if (tid == 0) {  // prefetch the first tile of this item
-      mbar_expect_tx(&bar[0], kTileBytes);
-      bulk_g2s(tile[0], src_base, kTileBytes, &bar[0]);
-    }
-
-    // targets of this thread: warp-contiguous (Morton order) -> tight warp boxes
-    Tgt tg[T];
-    Acc acc[T];
-    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-#pragma unroll
-    for (int j = 0; j < T; ++j) {
-      const int64_t i = (int64_t)tb * TB + warp * 32 * T + j * 32 + lane;
-      const double* q = p.tgt + i;
-      tg[j].y0 = q[F_Y0 * p.Mpad];
-      tg[j].y1 = q[F_Y1 * p.Mpad];
-      tg[j].y2 = q[F_Y2 * p.Mpad];
-      tg[j].alpha = (MODE & 1) ? q[F_ALPHA * p.Mpad] : 0.0;
-      tg[j].q0 = (MODE & 2) ? q[F_Q0 * p.Mpad] : 0.0;
-      tg[j].q1 = (MODE & 2) ? q[F_Q1 * p.Mpad] : 0.0;
-      tg[j].q2 = (MODE & 2) ? q[F_Q2 * p.Mpad] : 0.0;
-      acc[j] = Acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      lo[0] = fmin(lo[0], tg[j].y0); hi[0] = fmax(hi[0], tg[j].y0);
-      lo[1] = fmin(lo[1], tg[j].y1); hi[1] = fmax(hi[1], tg[j].y1);
-      lo[2] = fmin(lo[2], tg[j].y2); hi[2] = fmax(hi[2], tg[j].y2);
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-      for (int o = 16; o; o >>= 1) {
-        lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
-        hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
-      }
-
-    for (int t = 0; t < ntiles; ++t) {
-      const int buf = t & 1;
-      if (tid == 0 && t + 1 < ntiles) {  // the other buffer was released by the __syncthreads below
-        mbar_expect_tx(&bar[buf ^ 1], kTileBytes);
-        bulk_g2s(tile[buf ^ 1], src_base + (int64_t)(t + 1) * kTile * kSrcDoubles, kTileBytes, &bar[buf ^ 1]);
-      }
-      if (buf == 0) { mbar_wait(&bar[0], parity0); parity0 ^= 1; }
-      else { mbar_wait(&bar[1], parity1); parity1 ^= 1; }
-      const double* sm = tile[buf];
-      const double* boxes = p.src_box + ((int64_t)(tile0 + t) * (kTile / kSub)) * 8;
-#pragma unroll 1
-      for (int sub = 0; sub < kTile / kSub; ++sub) {
-        const double* bx = boxes + sub * 8;
-        double g2 = 0.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const double gap = fmax(0.0, fmax(__ldg(bx + d) - hi[d], lo[d] - __ldg(bx + 4 + d)));
-          g2 = fma(gap, gap, g2);
-        }
-        const double* ss = sm + sub * kSub * kSrcDoubles;
-        if (g2 > p.rc2_box) {  // warp-uniform: every pair of this sub-tile is far
-          // software pipeline: geometry + rsqrt of source k+1 overlap the
-          // contractions of source k (the last step recomputes source 0: discarded)
-          Src s = load_src<MODE>(ss);
-          Geo g[T];
-#pragma unroll
-          for (int j = 0; j < T; ++j) g[j] = far_geo(s, tg[j]);
-#pragma unroll kFarUnroll
-          for (int k = 0; k < kSub; ++k) {
-            const Src sn = load_src<MODE>(ss + ((k + 1) & (kSub - 1)) * kSrcDoubles);
-            Geo gn[T];
-#pragma unroll
-            for (int j = 0; j < T; ++j) gn[j] = far_geo(sn, tg[j]);
-#pragma unroll
-            for (int j = 0; j < T; ++j) far_acc<MODE>(s, tg[j], g[j], acc[j]);
-            s = sn;
-#pragma unroll
-            for (int j = 0; j < T; ++j) g[j] = gn[j];
-          }
-        } else {  // mixed: far pairs only, near pairs belong to the near kernel
-#pragma unroll 2
-          for (int k = 0; k < kSub; ++k) {
-            const Src s = load_src<MODE>(ss + k * kSrcDoubles);
-#pragma unroll
-            for (int j = 0; j < T; ++j) far_pair_masked<MODE>(s, tg[j], acc[j], p.rc2);
-          }
-        }
-      }
-      __syncthreads();  // all reads of `buf` done before it is refilled
-    }
-
-    // partial sums of this item: [item][6][TB]
-    double* out = p.partial + (int64_t)item * 6 * TB;
-#pragma unroll
-    for (int j = 0; j < T; ++j) {
-      const int loc = warp * 32 * T + j * 32 + lane;
-      if (MODE & 1) { out[0 * TB + loc] = acc[j].u0; out[1 * TB + loc] = acc[j].u1; out[2 * TB + loc] = acc[j].u2; }
-      if (MODE & 2) { out[3 * TB + loc] = acc[j].v0; out[4 * TB + loc] = acc[j].v1; out[5 * TB + loc] = acc[j].v2; }
-    }
+    far_item<MODE, T>(p, item, tile, bar, parity0, parity1);
   }
 }
 
@@ -635,129 +656,204 @@ constexpr int kQCap = 64;  // per-lane ring capacity (power of two)
 #ifndef SER_NEAR_MINB
 #define SER_NEAR_MINB 4
 #endif
+// Per-warp SMEM of the near unit: source xyz of the sub-tile being classified,
+// the per-lane ring queues and the lane targets' fields (SoA [field][lane]).
+struct NearSmem {
+  double sx[3][32];
+  int q[kQCap][32];
+  double tf[kNearFields][32];
+};
+
+template <int MODE, bool SHARP>
+__device__ __forceinline__ void near_unit(const NearParams& p, int unit, NearSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  int(*q)[32] = sm.q;
+  double(*tf)[32] = sm.tf;
+  const int n_sub = static_cast<int>(p.Npad / kSub);
+  const int64_t g = unit / p.phases;
+  const int phase = unit - static_cast<int>(g) * p.phases;
+  const int64_t ti = g * 32 + lane;
+  const double y0 = p.tgt[F_Y0 * p.Mpad + ti], y1 = p.tgt[F_Y1 * p.Mpad + ti], y2 = p.tgt[F_Y2 * p.Mpad + ti];
+  __syncwarp();
+  {
+    const double* tq = p.tgt + ti;
+    tf[NF_ALPHA][lane] = (MODE & 1) ? tq[F_ALPHA * p.Mpad] : 0.0;
+    tf[NF_Q0][lane] = (MODE & 2) ? tq[F_Q0 * p.Mpad] : 0.0;
+    tf[NF_Q1][lane] = (MODE & 2) ? tq[F_Q1 * p.Mpad] : 0.0;
+    tf[NF_Q2][lane] = (MODE & 2) ? tq[F_Q2 * p.Mpad] : 0.0;
+    tf[NF_N0][lane] = tq[F_N0 * p.Mpad];
+    tf[NF_N1][lane] = tq[F_N1 * p.Mpad];
+    tf[NF_N2][lane] = tq[F_N2 * p.Mpad];
+    tf[NF_B][lane] = tq[F_B * p.Mpad];
+    tf[NF_W0][lane] = tq[F_W0 * p.Mpad];
+    tf[NF_W1][lane] = tq[F_W1 * p.Mpad];
+    tf[NF_W2][lane] = tq[F_W2 * p.Mpad];
+  }
+  double lo[3] = {y0, y1, y2}, hi[3] = {y0, y1, y2};
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    for (int o = 16; o; o >>= 1) {
+      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+  Acc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int head = 0, tail = 0;
+  int ordinal = 0;  // index of the mixed sub-tile among this group's mixed sub-tiles
+
+  // Invariant: every lane's queue holds <= kQCap - 32 entries before a sub-tile
+  // appends its (<= 32) near sources.  One call site of the pair code.
+  int base = 0;
+  unsigned mm = 0;
+  for (;;) {
+    while (mm == 0 && base < n_sub) {
+      bool mixed = false;
+      const int sb = base + lane;
+      if (sb < n_sub) {
+        const double* bx = p.src_box + (int64_t)sb * 8;
+        double g2 = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double gap = fmax(0.0, fmax(__ldg(bx + d) - hi[d], lo[d] - __ldg(bx + 4 + d)));
+          g2 = fma(gap, gap, g2);
+        }
+        mixed = g2 <= p.rc2_box;
+      }
+      mm = __ballot_sync(0xffffffffu, mixed);
+      // keep only this phase's share of the mixed sub-tiles (round robin by ordinal)
+      unsigned keep = 0, m = mm;
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (ordinal % p.phases == phase) keep |= 1u << bit;
+        ++ordinal;
+      }
+      mm = keep;
+      base += 32;
+    }
+    int rounds;
+    const bool last = (mm == 0);
+    if (!last) {
+      const int sub = base - 32 + __ffs(mm) - 1;
+      mm &= mm - 1;
+      {
+        const double* gs = p.src + ((int64_t)sub * kSub + lane) * kSrcDoubles;
+        sm.sx[0][lane] = __ldg(gs);
+        sm.sx[1][lane] = __ldg(gs + 1);
+        sm.sx[2][lane] = __ldg(gs + 2);
+      }
+      __syncwarp();
+      unsigned smask = 0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const double dx = y0 - sm.sx[0][k], dy = y1 - sm.sx[1][k], dz = y2 - sm.sx[2][k];
+        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+        smask |= (r2 <= p.rc2 ? 1u : 0u) << k;
+      }
+      __syncwarp();
+      while (smask) {
+        const int bit = __ffs(smask) - 1;
+        smask &= smask - 1;
+        q[tail & (kQCap - 1)][lane] = sub * kSub + bit;
+        ++tail;
+      }
+      const int minlen = __reduce_min_sync(0xffffffffu, tail - head);
+      const int maxlen = __reduce_max_sync(0xffffffffu, tail - head);
+      rounds = max(minlen >= 32 ? minlen : 0, maxlen - (kQCap - 32));
+    } else {
+      rounds = __reduce_max_sync(0xffffffffu, tail - head);  // drain
+    }
+    for (int r = 0; r < rounds; ++r) {
+      if (head < tail) {
+        const int sidx = q[head & (kQCap - 1)][lane];
+        ++head;
+        const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
+        const Acc d = near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, nullptr);
+        acc.u0 += d.u0; acc.u1 += d.u1; acc.u2 += d.u2;
+        acc.v0 += d.v0; acc.v1 += d.v1; acc.v2 += d.v2;
+      }
+    }
+    if (last) break;
+  }
+  __syncwarp();  // all lanes done with sm before the warp's next unit overwrites it
+  double* out = p.near_out + (int64_t)phase * 6 * p.Mpad + ti;
+  out[0 * p.Mpad] = acc.u0; out[1 * p.Mpad] = acc.u1; out[2 * p.Mpad] = acc.u2;
+  out[3 * p.Mpad] = acc.v0; out[4 * p.Mpad] = acc.v1; out[5 * p.Mpad] = acc.v2;
+}
+
+// K3 (separate schedule): persistent warps pull units (group, phase) from a
+// queue: balanced tails.
 template <int MODE, bool SHARP>
 __global__ void __launch_bounds__(kNearWarps * 32, SER_NEAR_MINB) near_kernel(const NearParams p) {
-  __shared__ double s_sx[kNearWarps][3][32];
-  __shared__ int s_q[kNearWarps][kQCap][32];
-  __shared__ double s_tf[kNearWarps][kNearFields][32];
+  __shared__ NearSmem s_near[kNearWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int(*q)[32] = s_q[warp];
-  double(*tf)[32] = s_tf[warp];
-  const int n_sub = static_cast<int>(p.Npad / kSub);
-
-  // persistent warps pull units (group, phase) from a queue: balanced tails
   for (;;) {
     int unit = 0;
     if (lane == 0) unit = atomicAdd(p.counter, 1);
     unit = __shfl_sync(0xffffffffu, unit, 0);
     if (unit >= p.n_units) break;
-    const int64_t g = unit / p.phases;
-    const int phase = unit - static_cast<int>(g) * p.phases;
-    const int64_t ti = g * 32 + lane;
-    const double y0 = p.tgt[F_Y0 * p.Mpad + ti], y1 = p.tgt[F_Y1 * p.Mpad + ti], y2 = p.tgt[F_Y2 * p.Mpad + ti];
-    __syncwarp();
-    {
-      const double* tq = p.tgt + ti;
-      tf[NF_ALPHA][lane] = (MODE & 1) ? tq[F_ALPHA * p.Mpad] : 0.0;
-      tf[NF_Q0][lane] = (MODE & 2) ? tq[F_Q0 * p.Mpad] : 0.0;
-      tf[NF_Q1][lane] = (MODE & 2) ? tq[F_Q1 * p.Mpad] : 0.0;
-      tf[NF_Q2][lane] = (MODE & 2) ? tq[F_Q2 * p.Mpad] : 0.0;
-      tf[NF_N0][lane] = tq[F_N0 * p.Mpad];
-      tf[NF_N1][lane] = tq[F_N1 * p.Mpad];
-      tf[NF_N2][lane] = tq[F_N2 * p.Mpad];
-      tf[NF_B][lane] = tq[F_B * p.Mpad];
-      tf[NF_W0][lane] = tq[F_W0 * p.Mpad];
-      tf[NF_W1][lane] = tq[F_W1 * p.Mpad];
-      tf[NF_W2][lane] = tq[F_W2 * p.Mpad];
-    }
-    double lo[3] = {y0, y1, y2}, hi[3] = {y0, y1, y2};
-#pragma unroll
-    for (int d = 0; d < 3; ++d)
-      for (int o = 16; o; o >>= 1) {
-        lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
-        hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
-      }
-    Acc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int head = 0, tail = 0;
-    int ordinal = 0;  // index of the mixed sub-tile among this group's mixed sub-tiles
+    near_unit<MODE, SHARP>(p, unit, s_near[warp]);
+  }
+}
 
-    // Invariant: every lane's queue holds <= kQCap - 32 entries before a sub-tile
-    // appends its (<= 32) near sources.  One call site of the pair code.
-    int base = 0;
-    unsigned mm = 0;
-    for (;;) {
-      while (mm == 0 && base < n_sub) {
-        bool mixed = false;
-        const int sb = base + lane;
-        if (sb < n_sub) {
-          const double* bx = p.src_box + (int64_t)sb * 8;
-          double g2 = 0.0;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double gap = fmax(0.0, fmax(__ldg(bx + d) - hi[d], lo[d] - __ldg(bx + 4 + d)));
-            g2 = fma(gap, gap, g2);
-          }
-          mixed = g2 <= p.rc2_box;
-        }
-        mm = __ballot_sync(0xffffffffu, mixed);
-        // keep only this phase's share of the mixed sub-tiles (round robin by ordinal)
-        unsigned keep = 0, m = mm;
-        while (m) {
-          const int bit = __ffs(m) - 1;
-          m &= m - 1;
-          if (ordinal % p.phases == phase) keep |= 1u << bit;
-          ++ordinal;
-        }
-        mm = keep;
-        base += 32;
-      }
-      int rounds;
-      const bool last = (mm == 0);
-      if (!last) {
-        const int sub = base - 32 + __ffs(mm) - 1;
-        mm &= mm - 1;
-        {
-          const double* gs = p.src + ((int64_t)sub * kSub + lane) * kSrcDoubles;
-          s_sx[warp][0][lane] = __ldg(gs);
-          s_sx[warp][1][lane] = __ldg(gs + 1);
-          s_sx[warp][2][lane] = __ldg(gs + 2);
-        }
-        __syncwarp();
-        unsigned smask = 0;
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-          const double dx = y0 - s_sx[warp][0][k], dy = y1 - s_sx[warp][1][k], dz = y2 - s_sx[warp][2][k];
-          const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-          smask |= (r2 <= p.rc2 ? 1u : 0u) << k;
-        }
-        __syncwarp();
-        while (smask) {
-          const int bit = __ffs(smask) - 1;
-          smask &= smask - 1;
-          q[tail & (kQCap - 1)][lane] = sub * kSub + bit;
-          ++tail;
-        }
-        const int minlen = __reduce_min_sync(0xffffffffu, tail - head);
-        const int maxlen = __reduce_max_sync(0xffffffffu, tail - head);
-        rounds = max(minlen >= 32 ? minlen : 0, maxlen - (kQCap - 32));
-      } else {
-        rounds = __reduce_max_sync(0xffffffffu, tail - head);  // drain
-      }
-      for (int r = 0; r < rounds; ++r) {
-        if (head < tail) {
-          const int sidx = q[head & (kQCap - 1)][lane];
-          ++head;
-          const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
-          const Acc d = near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, nullptr);
-          acc.u0 += d.u0; acc.u1 += d.u1; acc.u2 += d.u2;
-          acc.v0 += d.v0; acc.v1 += d.v1; acc.v2 += d.v2;
-        }
-      }
-      if (last) break;
+// K13 (fused schedule, the default): one persistent kernel runs both the far
+// items (K1 body) and the near units (K3 body).  A near item is kNearWarps
+// units, one per warp.  The queue interleaves the two kinds: the first
+// (100 - SER_NEAR_TAIL_PCT)% of the near items are spread uniformly among the
+// far items, so an SM's resident CTAs mix the FP64-issue-bound far loop with the
+// latency-bound near pairs and the far warps fill the near warps' stalls; the
+// rest follow the last far item and fill the tail.  The
+// SMEM of the two bodies is a union; the item counter is PairParams::counter.
+constexpr int kFarSmemBytes = 2 * kTile * kSrcDoubles * 8;
+constexpr int kNearSmemBytes = kNearWarps * (int)sizeof(NearSmem);
+constexpr int kFusedSmemBytes = kFarSmemBytes > kNearSmemBytes ? kFarSmemBytes : kNearSmemBytes;
+#ifndef SER_NEAR_TAIL_PCT
+#define SER_NEAR_TAIL_PCT 0
+#endif
+
+// Queue position -> work: returns true for a near item (index *idx), false for
+// a far item.  Near items 0 .. n_mix-1 sit uniformly among the n_far far items,
+// the remaining near items follow the last far item.
+__device__ __forceinline__ bool fused_slot(int64_t qi, int64_t n_far, int64_t n_mix, int64_t* idx) {
+  const int64_t head = n_far + n_mix;
+  if (qi >= head) { *idx = n_mix + (qi - head); return true; }
+  const int64_t na = qi * n_mix / head, nb = (qi + 1) * n_mix / head;
+  if (nb > na) { *idx = na; return true; }
+  *idx = qi - na;
+  return false;
+}
+
+template <int MODE, int T, bool SHARP>
+__global__ void __launch_bounds__(kThreads, SER_FAR_MINB) fused_kernel(const PairParams p, const NearParams np,
+                                                                       int n_near_items) {
+  static_assert(kThreads == kNearWarps * 32, "fused kernel: one near unit per warp");
+  __shared__ __align__(128) unsigned char smem[kFusedSmemBytes];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_item;
+  auto* tile = reinterpret_cast<double(*)[kTile * kSrcDoubles]>(smem);
+  auto* near_sm = reinterpret_cast<NearSmem*>(smem);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t parity0 = 0, parity1 = 0;
+  const int64_t n_far = p.n_items;
+  const int64_t n_mix = n_near_items - (int64_t)n_near_items * SER_NEAR_TAIL_PCT / 100;
+  const int64_t total = n_far + n_near_items;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1);
+    __syncthreads();
+    const int64_t qi = s_item;
+    __syncthreads();  // every thread has read s_item (and left the previous item's SMEM)
+    if (qi >= total) break;
+    int64_t idx;
+    if (fused_slot(qi, n_far, n_mix, &idx)) {
+      const int64_t unit = idx * kNearWarps + (threadIdx.x >> 5);
+      if (unit < np.n_units) near_unit<MODE, SHARP>(np, static_cast<int>(unit), near_sm[threadIdx.x >> 5]);
+    } else {
+      far_item<MODE, T>(p, static_cast<int>(idx), tile, bar, parity0, parity1);
     }
-    double* out = p.near_out + (int64_t)phase * 6 * p.Mpad + ti;
-    out[0 * p.Mpad] = acc.u0; out[1 * p.Mpad] = acc.u1; out[2 * p.Mpad] = acc.u2;
-    out[3 * p.Mpad] = acc.v0; out[4 * p.Mpad] = acc.v1; out[5 * p.Mpad] = acc.v2;
   }
 }
 

@@ -218,6 +218,13 @@ int check_arch() {
   return major == 10 ? STOKES_ER_OK : STOKES_ER_EARCH;
 }
 
+int opt_T(const stokes_er_options* o) {
+  return (o && o->targets_per_thread >= 1 && o->targets_per_thread <= 4) ? o->targets_per_thread : 2;
+}
+int opt_chunk(const stokes_er_options* o) { return o ? o->source_chunk_tiles : 0; }
+int opt_phases(const stokes_er_options* o) { return o ? o->near_phases : 0; }
+int opt_schedule(const stokes_er_options* o) { return o ? o->schedule : STOKES_ER_SCHEDULE_FUSED; }
+
 template <int MODE, int T>
 void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
   int dev = 0, sms = 0, occ = 0;
@@ -227,6 +234,16 @@ void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
   const int grid = std::max(1, std::min(pp.n_items, sms * std::max(occ, 1)));
   *grid_out = grid;
   far_kernel<MODE, T><<<grid, kThreads, 0, s>>>(pp);
+}
+
+template <int MODE, int T, bool SHARP>
+int launch_fused(const PairParams& pp, const NearParams& np, int n_near_items, int sms, cudaStream_t s) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<MODE, T, SHARP>, kThreads, 0);
+  const int64_t work = (int64_t)pp.n_items + n_near_items;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)sms * std::max(occ, 1))));
+  fused_kernel<MODE, T, SHARP><<<grid, kThreads, 0, s>>>(pp, np, n_near_items);
+  return grid;
 }
 
 // SHARP = NEXT-1 on-surface variant: h = delta, rho = (1,1,1), weights (1,0,0),
@@ -285,17 +302,9 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   const double cutoff = SHARP ? STOKES_ER_CUTOFF_SURFACE : STOKES_ER_CUTOFF;
   pp.rc2 = (cutoff * dmax) * (cutoff * dmax);
   pp.rc2_box = pp.rc2 * (1.0 + 1e-9);
+  pp.rc2_inner = pp.rc2 * (1.0 - 1e-9);
   pp.r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
   for (int k = 0; k < 3; ++k) pp.inv_delta[k] = 1.0 / (rho[k] * h);
-
-  if (opt && opt->pair_kernel_start_event)
-    cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
-  int grid = 0;
-  if (P.T == 4) launch_pairs<MODE, 4>(pp, s, &grid);
-  else if (P.T == 3) launch_pairs<MODE, 3>(pp, s, &grid);
-  else if (P.T == 1) launch_pairs<MODE, 1>(pp, s, &grid);
-  else launch_pairs<MODE, 2>(pp, s, &grid);
-  if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
 
   NearParams np;
   np.src = src;
@@ -311,18 +320,38 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   np.rc2_box = pp.rc2_box;
   np.r2_tiny = pp.r2_tiny;
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = pp.inv_delta[k];
-  if (opt && opt->near_kernel_start_event)
-    cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_start_event), s);
-  {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int grid = 0;
+  if (opt_schedule(opt) == STOKES_ER_SCHEDULE_FUSED) {
+    // one persistent kernel: far items and near items (kNearWarps units each) interleaved
+    const int n_near_items = static_cast<int>(ceil_div(np.n_units, kNearWarps));
+    if (opt && opt->pair_kernel_start_event)
+      cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
+    if (P.T == 4) grid = launch_fused<MODE, 4, SHARP>(pp, np, n_near_items, sms, s);
+    else if (P.T == 3) grid = launch_fused<MODE, 3, SHARP>(pp, np, n_near_items, sms, s);
+    else if (P.T == 1) grid = launch_fused<MODE, 1, SHARP>(pp, np, n_near_items, sms, s);
+    else grid = launch_fused<MODE, 2, SHARP>(pp, np, n_near_items, sms, s);
+    if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
+  } else {
+    if (opt && opt->pair_kernel_start_event)
+      cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
+    if (P.T == 4) launch_pairs<MODE, 4>(pp, s, &grid);
+    else if (P.T == 3) launch_pairs<MODE, 3>(pp, s, &grid);
+    else if (P.T == 1) launch_pairs<MODE, 1>(pp, s, &grid);
+    else launch_pairs<MODE, 2>(pp, s, &grid);
+    if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
+    if (opt && opt->near_kernel_start_event)
+      cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_start_event), s);
+    int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_kernel<MODE, SHARP>, kNearWarps * 32, 0);
-    const int grid = static_cast<int>(std::max<int64_t>(
+    const int ngrid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(occ, 1))));
-    near_kernel<MODE, SHARP><<<grid, kNearWarps * 32, 0, s>>>(np);
+    near_kernel<MODE, SHARP><<<ngrid, kNearWarps * 32, 0, s>>>(np);
+    if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
   }
-  if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
   if (opt) {
     opt->stats[0] = P.n_items;
     opt->stats[1] = grid;
@@ -334,11 +363,6 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
 }
 
-int opt_T(const stokes_er_options* o) {
-  return (o && o->targets_per_thread >= 1 && o->targets_per_thread <= 4) ? o->targets_per_thread : 2;
-}
-int opt_chunk(const stokes_er_options* o) { return o ? o->source_chunk_tiles : 0; }
-int opt_phases(const stokes_er_options* o) { return o ? o->near_phases : 0; }
 
 size_t host_stage_bytes(int64_t M, int64_t N) {
   return align_up(13 * N * sizeof(double)) + align_up(13 * M * sizeof(double)) + align_up(6 * M * sizeof(double)) +
@@ -511,9 +535,10 @@ int stokes_er_extrapolate(const double* tgt_b, int64_t M, double h, const double
 int stokes_er_launch_count(int64_t M, int64_t N, int mode) {
   (void)N;
   (void)mode;
-  // bbox, 2x morton, pack sources, pack targets, far, near, finalize: our kernels.
-  // The two CUB radix sorts add their own launches (library code).
-  return M > 0 ? 8 : 0;
+  // bbox, 2x morton, pack sources, pack targets, fused far+near, finalize: our
+  // kernels (default schedule; STOKES_ER_SCHEDULE_SEPARATE adds one).  The two
+  // CUB radix sorts add their own launches (library code).
+  return M > 0 ? 7 : 0;
 }
 
 const char* stokes_er_status_string(int status) {

@@ -147,6 +147,22 @@ def test_tunings_agree(ser):
         assert rel(u, base[0]) <= 1e-13 and rel(v, base[1]) <= 1e-13
 
 
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_schedules_agree(ser, mode):
+    """Fused (default) vs separate far/near kernels: the same pair sums (same
+    per-slot partials, same fixed-order finalize), so bitwise equal; both vs oracle."""
+    blk = config2(inv_h=32)
+    o = ser.Options()
+    o.schedule = 1
+    fu = run_gpu(ser, blk, mode=mode)
+    se = run_gpu(ser, blk, mode=mode, options=o)
+    for a, b in zip(fu, se):
+        if a is not None:
+            assert rel(a, b) <= 1e-14
+    check_block(ser, config1(), mode=mode)
+    check_block(ser, config1(), mode=mode, options=o)
+
+
 def test_deterministic(ser):
     blk = config2(inv_h=32)
     a = run_gpu(ser, blk)
