@@ -128,22 +128,31 @@ __device__ __forceinline__ uint32_t spread10(uint32_t v) {
   return v;
 }
 
-// One CTA: min/max over sources and targets -> box[0..2] lo, box[3..5] hi.
+// Bounding box of sources and targets as order-preserving int64 keys:
+// key(v) = bits(v) ^ ((bits(v) >> 63) & 0x7fff...) orders like the doubles, so
+// a grid-wide reduction is atomicMin/atomicMax on long long.  box[0..2] = lo
+// keys (pre-set to 0x7f7f.. by a memset), box[3..5] = hi keys (0x8080..).
+__device__ __forceinline__ long long dkey(double v) {
+  const long long b = __double_as_longlong(v);
+  return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
+}
+__device__ __forceinline__ double dkey_inv(long long k) {
+  return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffLL));
+}
 __global__ void bbox_kernel(const double* __restrict__ sx, int64_t N, const double* __restrict__ tx, int64_t M,
-                            double* __restrict__ box) {
+                            long long* __restrict__ box) {
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int64_t i = threadIdx.x; i < N; i += blockDim.x)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N + M; i += stride) {
+    const double* x = i < N ? sx + i : tx + (i - N);
+    const int64_t n = i < N ? N : M;
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const double v = sx[d * N + i];
+      const double v = x[d * n];
       lo[d] = fmin(lo[d], v);
       hi[d] = fmax(hi[d], v);
     }
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x)
-    for (int d = 0; d < 3; ++d) {
-      const double v = tx[d * M + i];
-      lo[d] = fmin(lo[d], v);
-      hi[d] = fmax(hi[d], v);
-    }
+  }
   __shared__ double red[32][6];
   for (int d = 0; d < 3; ++d)
     for (int o = 16; o; o >>= 1) {
@@ -158,19 +167,21 @@ __global__ void bbox_kernel(const double* __restrict__ sx, int64_t N, const doub
     const int nw = blockDim.x >> 5;
     double v = red[0][threadIdx.x];
     for (int i = 1; i < nw; ++i) v = threadIdx.x < 3 ? fmin(v, red[i][threadIdx.x]) : fmax(v, red[i][threadIdx.x]);
-    box[threadIdx.x] = v;
+    if (threadIdx.x < 3) atomicMin(box + threadIdx.x, dkey(v));
+    else atomicMax(box + threadIdx.x, dkey(v));
   }
 }
 
-__global__ void morton_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ box,
+__global__ void morton_kernel(const double* __restrict__ x, int64_t n, const long long* __restrict__ box,
                               uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint32_t key = 0;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    const double ext = fmax(box[3 + d] - box[d], 1e-300);
-    double s = (x[d * n + i] - box[d]) / ext * 1023.0;
+    const double blo = dkey_inv(box[d]), bhi = dkey_inv(box[3 + d]);
+    const double ext = fmax(bhi - blo, 1e-300);
+    double s = (x[d * n + i] - blo) / ext * 1023.0;
     s = fmin(fmax(s, 0.0), 1023.0);
     key |= spread10(static_cast<uint32_t>(s)) << d;
   }

@@ -253,7 +253,7 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
              const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
              const double* rho, double* out_u, double* out_v, char* ws, const Plan& P, cudaStream_t s,
              stokes_er_options* opt) {
-  double* box = reinterpret_cast<double*>(ws + P.off_box);
+  long long* box = reinterpret_cast<long long*>(ws + P.off_box);
   uint32_t* skin = reinterpret_cast<uint32_t*>(ws + P.off_skin);
   uint32_t* skout = reinterpret_cast<uint32_t*>(ws + P.off_skout);
   int32_t* svin = reinterpret_cast<int32_t*>(ws + P.off_svin);
@@ -270,7 +270,10 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   double* near_out = reinterpret_cast<double*>(ws + P.off_near);
   int* counter = reinterpret_cast<int*>(ws + P.off_counter);
 
-  bbox_kernel<<<1, 1024, 0, s>>>(sx, N, ty, M, box);
+  if (cudaMemsetAsync(box, 0x7f, 3 * sizeof(long long), s) != cudaSuccess ||
+      cudaMemsetAsync(box + 3, 0x80, 3 * sizeof(long long), s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  bbox_kernel<<<static_cast<int>(std::min<int64_t>(2 * 148, ceil_div(N + M, 256))), 256, 0, s>>>(sx, N, ty, M, box);
   morton_kernel<<<ceil_div(N, 256), 256, 0, s>>>(sx, N, box, skin, svin);
   morton_kernel<<<ceil_div(M, 256), 256, 0, s>>>(ty, M, box, tkin, tvin);
   size_t cb = P.cub_bytes;
