@@ -70,7 +70,8 @@ typedef enum {
                                finite, rho not positive strictly increasing, bad mode   */
   STOKES_ER_ECUDA = 2,      /* a CUDA runtime call or kernel launch failed              */
   STOKES_ER_EWORKSPACE = 3, /* workspace NULL or smaller than stokes_er_workspace_bytes */
-  STOKES_ER_EARCH = 4       /* current device is not compute capability 10.x (sm_100)   */
+  STOKES_ER_EARCH = 4,      /* current device is not compute capability 10.x (sm_100)   */
+  STOKES_ER_ENOCONV = 5     /* stokes_er_twodrop_solve: max_iter reached above tol      */
 } stokes_er_status;
 
 /* Bytes of device workspace needed by stokes_er_eval / stokes_er_eval_deltas. */
@@ -189,6 +190,79 @@ int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const dou
                       const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
                       int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
                       void* stream, stokes_er_options* options);
+
+/* ===================================================================== NEXT-2
+ * Two-drop interfacial Stokes flow (Sec. 4.3): the
+ * interface velocity u on two drops solves the integral equation (35)
+ * (`IE-2Surf`), for x0 on drop b, m != b:
+ *
+ *   (lambda_b + 1) u(x0) = -(1/(4 pi mu0)) sum_m int_m S [f] dS + sum_m (lambda_m - 1)/(4 pi) int_m T u n dS
+ *
+ * written with this library's evaluators (which carry 1/(8 pi)) as
+ *
+ *   A u|_b = (lambda_b + 1) u_b - 2 (lambda_b - 1) DL_bb[u_b] - 2 (lambda_m - 1) DL_bm[u_m]
+ *   rhs_b  = -(2/mu0) (SL_bb[[f]_b] + SL_bm[[f]_m])
+ *
+ * Self blocks (bb) are stokes_er_eval_onsurface at delta_self (paper: 3h;
+ * DL_bb is the principal value, chi = 1/2); cross blocks (bm) are
+ * stokes_er_eval with rho (paper: 3,4,5) and targets = drop b's nodes whose
+ * closest point x0 on drop m the caller supplies (b', n0, [f]_m(x0)).  The
+ * cross DL subtracts u_m(x0), which is not a node value: it is the value at
+ * x0 of the least-squares polynomial of total degree <= 4 in tangent-plane
+ * coordinates over drop m's nodes within 3.5 h of x0 (R20).  The
+ * solve is full GMRES (modified Gram-Schmidt, no restart) from u = 0 until
+ * ||rhs - A u|| <= tol ||rhs|| (R21).
+ *
+ * Vectors u, rhs, A u: [3 N_1 + 3 N_2] device, drop 1 then drop 2, each [3][N_b].
+ * Workspace: caller-owned device memory of stokes_er_twodrop_workspace_bytes;
+ * stokes_er_twodrop_setup writes the interpolation stencils into it, and the
+ * other calls read them (same drops, cross, params and workspace).
+ * rhs/apply only enqueue on `stream`; setup and solve synchronize `stream`.
+ * Errors as above; EINVAL also when a stencil finds fewer than 15 or more
+ * than STOKES_ER_INTERP_KMAX nodes (setup), ENOCONV (5) when solve reaches
+ * max_iter above tol (out_u then holds the last iterate).
+ */
+#define STOKES_ER_INTERP_KMAX 192
+
+typedef struct {
+  int64_t N;              /* quadrature nodes of the drop                          */
+  const double* xyz;      /* [3][N] nodes                                          */
+  const double* normal;   /* [3][N] outward unit normals                           */
+  const double* weight;   /* [N]    quadrature weights                             */
+  const double* f;        /* [3][N] interface force jump [f] at the nodes          */
+  double lambda;          /* viscosity ratio mu_drop / mu0                         */
+} stokes_er_drop;
+
+typedef struct {          /* cross[b]: targets = nodes of drop b, sources = drop 1-b */
+  const double* b;        /* [N_b] signed distance of the node to drop 1-b (> 0)    */
+  const double* x0d;      /* [6][N_b]: n0 at the closest point x0 on drop 1-b (3),
+                                       [f]_{1-b}(x0) (3); x0 = y - b n0              */
+} stokes_er_cross;
+
+typedef struct {
+  double h;               /* grid spacing of both drops                            */
+  double rho[3];          /* cross blocks: delta_k = rho_k h, strictly increasing  */
+  double delta_self;      /* self blocks: the s# smoothing length                  */
+  double mu0;             /* exterior viscosity                                    */
+  double tol;             /* GMRES relative residual                               */
+  int max_iter;           /* Krylov dimension cap, 1..512                          */
+} stokes_er_twodrop_params;
+
+size_t stokes_er_twodrop_workspace_bytes(int64_t N1, int64_t N2, int max_iter);
+int stokes_er_twodrop_setup(const stokes_er_drop drops[2], const stokes_er_cross cross[2],
+                            const stokes_er_twodrop_params* params, void* workspace, size_t workspace_bytes,
+                            void* stream);
+int stokes_er_twodrop_rhs(const stokes_er_drop drops[2], const stokes_er_cross cross[2],
+                          const stokes_er_twodrop_params* params, double* out_rhs, void* workspace,
+                          size_t workspace_bytes, void* stream);
+int stokes_er_twodrop_apply(const stokes_er_drop drops[2], const stokes_er_cross cross[2],
+                            const stokes_er_twodrop_params* params, const double* u, double* out_Au,
+                            void* workspace, size_t workspace_bytes, void* stream);
+/* out_iters: Arnoldi steps taken; out_res_host: [max_iter] relative residual
+ * estimate after each step (host, may be NULL). */
+int stokes_er_twodrop_solve(const stokes_er_drop drops[2], const stokes_er_cross cross[2],
+                            const stokes_er_twodrop_params* params, double* out_u, int* out_iters,
+                            double* out_res_host, void* workspace, size_t workspace_bytes, void* stream);
 
 const char* stokes_er_status_string(int status);
 int stokes_er_abi_version(void);

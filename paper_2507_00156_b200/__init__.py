@@ -204,3 +204,81 @@ def evaluate_block(block, mode=BOTH, device="cuda", **kw):
 
 Options = _lib.Options
 StokesERError = _lib.StokesERError
+
+
+class TwoDropSolver:
+    """NEXT-2 (Sec. 4.3): IE (35) on two drops through the C ABI
+    (stokes_er_twodrop_*).  Holds the device inputs and the workspace in which
+    stokes_er_twodrop_setup leaves the interpolation stencils.
+
+    drops: two dicts with device tensors xyz (3,N), normal (3,N), weight (N,), f (3,N)
+    and float lam; cross: two dicts with b (N_b,) and x0d (6,N_b) (n0, [f](x0)) of
+    drop b's nodes seen from drop 1-b (include/stokes_er.h)."""
+
+    def __init__(self, drops, cross, h, rho, delta_self, mu0=1.0, tol=1e-10, max_iter=100, stream=None):
+        torch = _torch()
+        self.L = _lib.load()
+        self._keep = (drops, cross)
+        self.N = [int(d["xyz"].shape[1]) for d in drops]
+        self.n = 3 * sum(self.N)
+        self.device = drops[0]["xyz"].device
+        for b, d in enumerate(drops):
+            N = self.N[b]
+            for k, shp in (("xyz", (3, N)), ("normal", (3, N)), ("weight", (N,)), ("f", (3, N))):
+                _check_dev(f"drops[{b}].{k}", d[k], shp)
+            _check_dev(f"cross[{b}].b", cross[b]["b"], (N,))
+            _check_dev(f"cross[{b}].x0d", cross[b]["x0d"], (6, N))
+        self.drops = (_lib.Drop * 2)(*[_lib.Drop(self.N[b], _ptr(d["xyz"]), _ptr(d["normal"]), _ptr(d["weight"]),
+                                                 _ptr(d["f"]), float(d["lam"])) for b, d in enumerate(drops)])
+        self.cross = (_lib.Cross * 2)(*[_lib.Cross(_ptr(c["b"]), _ptr(c["x0d"])) for c in cross])
+        self.params = _lib.TwoDropParams(float(h), (ctypes.c_double * 3)(*[float(r) for r in rho]),
+                                         float(delta_self), float(mu0), float(tol), int(max_iter))
+        nbytes = int(self.L.stokes_er_twodrop_workspace_bytes(self.N[0], self.N[1], int(max_iter)))
+        if nbytes == 0:
+            raise ValueError("stokes_er_twodrop_workspace_bytes: invalid sizes")
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.stream = stream
+        _lib.check("stokes_er_twodrop_setup",
+                   self.L.stokes_er_twodrop_setup(self.drops, self.cross, ctypes.byref(self.params), _ptr(self.ws),
+                                                  nbytes, _stream_handle(stream)))
+
+    def _common(self):
+        return self.drops, self.cross, ctypes.byref(self.params)
+
+    def rhs(self, out=None):
+        torch = _torch()
+        out = out if out is not None else torch.empty(self.n, dtype=torch.float64, device=self.device)
+        _lib.check("stokes_er_twodrop_rhs", self.L.stokes_er_twodrop_rhs(
+            *self._common(), _ptr(out), _ptr(self.ws), int(self.ws.numel()), _stream_handle(self.stream)))
+        return out
+
+    def apply(self, u, out=None):
+        torch = _torch()
+        _check_dev("u", u, (self.n,))
+        out = out if out is not None else torch.empty(self.n, dtype=torch.float64, device=self.device)
+        _lib.check("stokes_er_twodrop_apply", self.L.stokes_er_twodrop_apply(
+            *self._common(), _ptr(u), _ptr(out), _ptr(self.ws), int(self.ws.numel()), _stream_handle(self.stream)))
+        return out
+
+    def solve(self, out=None):
+        """Returns (u (n,), iterations, residual history list)."""
+        torch = _torch()
+        out = out if out is not None else torch.empty(self.n, dtype=torch.float64, device=self.device)
+        iters = ctypes.c_int(0)
+        hist = (ctypes.c_double * self.params.max_iter)()
+        st = self.L.stokes_er_twodrop_solve(*self._common(), _ptr(out), ctypes.byref(iters), hist, _ptr(self.ws),
+                                            int(self.ws.numel()), _stream_handle(self.stream))
+        _lib.check("stokes_er_twodrop_solve", st)
+        return out, int(iters.value), [float(hist[i]) for i in range(iters.value)]
+
+
+def twodrop_solver(td, device="cuda", max_iter=100, stream=None):
+    """TwoDropSolver from a workloads.twodrop.TwoDrop input set (numpy arrays -> device)."""
+    torch = _torch()
+    dev = lambda a: torch.from_numpy(a).to(device)
+    drops = [dict(xyz=dev(d.x), normal=dev(d.n), weight=dev(d.w), f=dev(d.f), lam=d.lam) for d in td.drops]
+    cross = []
+    for c in td.cross:
+        import numpy as np
+        cross.append(dict(b=dev(c.b), x0d=dev(np.ascontiguousarray(np.concatenate([c.n0, c.f0], axis=0)))))
+    return TwoDropSolver(drops, cross, td.h, td.rho, td.delta_self, 1.0, td.tol, max_iter, stream)

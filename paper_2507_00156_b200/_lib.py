@@ -11,7 +11,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("STOKES_ER_LIB") or os.path.join(PKG, "libstokes_er.so")
 
-STATUS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "EWORKSPACE", 4: "EARCH"}
+STATUS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "EWORKSPACE", 4: "EARCH", 5: "ENOCONV"}
 
 _dp = ctypes.c_void_p  # device or host pointers are passed as raw addresses
 _i64 = ctypes.c_int64
@@ -31,9 +31,24 @@ class Options(ctypes.Structure):
                 ("schedule", ctypes.c_int)]
 
 
+class Drop(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("xyz", ctypes.c_void_p), ("normal", ctypes.c_void_p),
+                ("weight", ctypes.c_void_p), ("f", ctypes.c_void_p), ("lam", ctypes.c_double)]
+
+
+class Cross(ctypes.Structure):
+    _fields_ = [("b", ctypes.c_void_p), ("x0d", ctypes.c_void_p)]
+
+
+class TwoDropParams(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_double), ("rho", ctypes.c_double * 3), ("delta_self", ctypes.c_double),
+                ("mu0", ctypes.c_double), ("tol", ctypes.c_double), ("max_iter", ctypes.c_int)]
+
+
 EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_er_eval", "stokes_er_eval_ex", "stokes_er_host_workspace_bytes",
            "stokes_er_eval_host", "stokes_er_eval_deltas", "stokes_er_eval_onsurface", "stokes_er_extrapolate", "stokes_er_launch_count",
-           "stokes_er_status_string", "stokes_er_abi_version"]
+           "stokes_er_status_string", "stokes_er_abi_version", "stokes_er_twodrop_workspace_bytes",
+           "stokes_er_twodrop_setup", "stokes_er_twodrop_rhs", "stokes_er_twodrop_apply", "stokes_er_twodrop_solve"]
 
 _lib = None
 
@@ -74,6 +89,18 @@ def load():
     L.stokes_er_status_string.argtypes = [ctypes.c_int]
     L.stokes_er_status_string.restype = ctypes.c_char_p
     L.stokes_er_abi_version.restype = ctypes.c_int
+    td = [ctypes.POINTER(Drop), ctypes.POINTER(Cross), ctypes.POINTER(TwoDropParams)]
+    L.stokes_er_twodrop_workspace_bytes.argtypes = [_i64, _i64, ctypes.c_int]
+    L.stokes_er_twodrop_workspace_bytes.restype = ctypes.c_size_t
+    L.stokes_er_twodrop_setup.argtypes = td + [_dp, ctypes.c_size_t, _dp]
+    L.stokes_er_twodrop_setup.restype = ctypes.c_int
+    L.stokes_er_twodrop_rhs.argtypes = td + [_dp, _dp, ctypes.c_size_t, _dp]
+    L.stokes_er_twodrop_rhs.restype = ctypes.c_int
+    L.stokes_er_twodrop_apply.argtypes = td + [_dp, _dp, _dp, ctypes.c_size_t, _dp]
+    L.stokes_er_twodrop_apply.restype = ctypes.c_int
+    L.stokes_er_twodrop_solve.argtypes = td + [_dp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
+                                               _dp, ctypes.c_size_t, _dp]
+    L.stokes_er_twodrop_solve.restype = ctypes.c_int
     _lib = L
     return L
 

@@ -18,6 +18,11 @@ def sources():
                   + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
+def cu_sources():
+    """Translation units of libstokes_er.so."""
+    return [os.path.join(PKG, "csrc", f) for f in ("stokes_er.cu", "twodrop.cu")]
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -29,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", tmp, os.path.join(PKG, "csrc", "stokes_er.cu")]
+    cmd = [NVCC, *FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", tmp, *cu_sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stderr}")

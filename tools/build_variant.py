@@ -16,8 +16,7 @@ name, defs = sys.argv[1], sys.argv[2:]
 out_dir = os.path.join(ROOT, "build", "variants")
 os.makedirs(out_dir, exist_ok=True)
 out = os.path.join(out_dir, f"libstokes_er_{name}.so")
-cmd = [b.NVCC, *b.FLAGS, *defs, "-I" + os.path.join(ROOT, "include"), "-o", out,
-       os.path.join(b.PKG, "csrc", "stokes_er.cu")]
+cmd = [b.NVCC, *b.FLAGS, *defs, "-I" + os.path.join(ROOT, "include"), "-o", out, *b.cu_sources()]
 res = subprocess.run(cmd, capture_output=True, text=True)
 if res.returncode:
     sys.exit(res.stderr)
