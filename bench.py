@@ -37,6 +37,7 @@ UNIT = "pairs/s"
 # Stated per-pair FLOP counts: algorithmic
 # flops with rsqrt/erf/exp = 1; FMA = 2.
 F_FAR_ALG = 57
+F_FAR_SL, F_FAR_DL = 35, 33  # SL-only / DL-only far pairs
 F_NEAR_ALG = 180
 F_FAR_ISSUED = 64   # ncu-countable FP64 flops (2*DFMA + DMUL + DADD) of far_pair<3> (41 instructions)
 F_NEAR_ISSUED = 378  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r01/ncu_full_v8: 144 DFMA, 60 DMUL, 30 DADD)
@@ -56,6 +57,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
     ap.add_argument("--near-phases", type=int, default=0)
+    ap.add_argument("--workload", choices=["eval", "twodrop"], default="eval",
+                    help="eval: one stokes_er_eval of BASELINE.json config --config (default); "
+                         "twodrop: one GMRES solve of the NEXT-2 two-drop IE (35) at 1/h = --inv-h")
     ap.add_argument("--schedule", choices=["fused", "separate"], default="fused",
                     help="fused: one persistent kernel, far items and near items from one interleaved "
                          "queue (default); separate: far kernel then near kernel")
@@ -196,11 +200,150 @@ def cpu_baseline(block):
                       f"(paper's shared-far-field algorithm), {dt:.1f} s wall"}
 
 
+def twodrop_launches(it: int) -> int:
+    """Our kernel launches in one stokes_er_twodrop_solve that took `it` Krylov steps."""
+    per_eval = 7
+    n = 4 * per_eval + 2 + 2                # rhs: 4 block evals + 2 combines, norm (2)
+    for j in range(it):
+        n += 4 * per_eval + 2 + 2           # operator: 4 evals, 2 interpolations, 2 combines
+        n += 3 * (j + 1) + 3                # MGS: dot (2) + update (1) per basis vector; norm + scale
+    return n + it                           # u = V y
+
+def run_twodrop(args, rank, world):
+    """NEXT-2 bench: one step = one full GMRES solve of IE (35) (Sec. 4.3)
+    on the two drops at 1/h = args.inv_h through stokes_er_twodrop_solve: 4 block
+    evaluations per Krylov step + the right-hand side, tol 1e-10.  value = block
+    pair interactions per second (4 blocks x (iterations + 1) x N_b N_m pairs / time)."""
+    import torch
+
+    import paper_2507_00156_b200 as ser
+    from workloads.twodrop import twodrop
+
+    dist = None
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    td = twodrop(args.inv_h)
+    N = [d.N for d in td.drops]
+    s = ser.twodrop_solver(td, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    K, W = args.steps, args.warmup
+    iters = []
+    for _ in range(W):
+        flush.zero_()
+        s.solve()
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(K):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _, it, hist = s.solve()
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+            iters.append(it)
+    from paper_2507_00156_b200.sharding import max_over_ranks
+    total_s = max_over_ranks(sum(ms) / 1e3, dev)
+    pairs_matvec = sum(N[i] * N[j] for i in range(2) for j in range(2))
+    it = iters[-1]
+    pairs = pairs_matvec * (it + 1)
+    value = world * pairs * K / total_s
+    # end to end through the public API: host arrays -> device, setup, solve, u -> host
+    e_ms = []
+    host = [np.ascontiguousarray(a) for d in td.drops for a in (d.x, d.n, d.w, d.f)]
+    h2d = sum(a.nbytes for a in host) + sum(c.b.nbytes + c.n0.nbytes + c.f0.nbytes for c in td.cross)
+    for _ in range(max(3, K // 4)):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        s2 = ser.twodrop_solver(td, device=dev)
+        u, _, _ = s2.solve()
+        u_host = u.cpu()
+        b.record()
+        b.synchronize()
+        e_ms.append(a.elapsed_time(b))
+    e_total = max_over_ranks(sum(e_ms) / 1e3, dev)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return None
+    # algorithmic flops of the solve's block evaluations (near pairs by KD-tree per block)
+    from scipy.spatial import cKDTree
+    near = 0
+    for b in range(2):
+        tb = cKDTree(td.drops[b].x.T)
+        near += tb.count_neighbors(cKDTree(td.drops[b].x.T), 7.0 * td.delta_self)        # self: s#, c = 7
+        near += tb.count_neighbors(cKDTree(td.drops[1 - b].x.T), 6.0 * max(td.rho) * td.h)  # cross: c = 6
+    near *= (it + 1)
+    # the rhs evaluates SL-only blocks, every Krylov step DL-only blocks: count every
+    # pair (near ones included, a lower bound) at the far-pair flops of its mode
+    flops = pairs_matvec * (F_FAR_SL + F_FAR_DL * it)
+    peak = SMS * FP64_LANES_PER_SM * 2 * 1965.0 * 1e6 / 1e12
+    achieved = flops / (total_s / K) / 1e12
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle.twodrop import TwoDropOracle
+        tds = twodrop(min(args.inv_h, 16))
+        o = TwoDropOracle(tds)
+        vec = np.random.default_rng(0).uniform(-1, 1, tds.n_unknowns)
+        t0 = time.perf_counter()
+        o.apply(vec)
+        dt = time.perf_counter() - t0
+        Ns = [d.N for d in tds.drops]
+        cpu = {"value": sum(Ns[i] * Ns[j] for i in range(2) for j in range(2)) / dt, "unit": UNIT,
+               "cores": __import__("oracle").max_threads(), "kind": "oracle",
+               "sample": f"one operator application (4 blocks) of the oracle at 1/h = {min(args.inv_h, 16)} "
+                         f"(N = {Ns[0]} per drop), localized mode, {dt:.1f} s wall"}
+    line = {"metric": "two-drop IE (35) GMRES solve: block pair interactions/sec (SL+DL blocks, tol 1e-10)",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"twodrop_h1/{args.inv_h}", "N_per_drop": N, "iterations": it,
+                       "block_evals_per_solve": 4 * (it + 1), "pairs_per_solve": pairs,
+                       "near_pairs_per_solve": int(near), "rho_cross": list(td.rho), "delta_self_over_h": 3.0,
+                       "eps": td.meta["eps"], "lambda": list(td.meta["lambda"]), "tol": td.tol,
+                       "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "whole solve (4 (it+1) stokes_er_eval calls + GMRES vector ops) over its "
+                                   "device time: every pair at the far-pair algorithmic flops of its mode, "
+                                   f"{F_FAR_SL} (SL, rhs) / {F_FAR_DL} (DL, Krylov steps); a lower bound",
+                         "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz"},
+            "clocks": clk.summary(),
+            "gpu_launches": K * twodrop_launches(it),
+            "gpu_launches_note": "per solve: rhs (4 evals x 7 + 2 combines) + per Krylov step j (4 evals x 7 + "
+                                 "2 interpolations + 2 combines + (j+1) MGS dots/updates x 3 + norm/scale 3) + "
+                                 "final combination (our kernels; CUB sort launches not counted)",
+            "e2e": {"value": world * pairs * len(e_ms) / e_total, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(u_host.numel() * 8),
+                    "note": "host arrays -> device, stencil setup, solve, u -> host"}}
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if dist is not None:
+        dist.destroy_process_group()
+    return line
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.workload == "twodrop" and args.impl == "ours":
+        line = run_twodrop(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
 
     if args.impl == "reference":
         line = run_reference(args, rank, world)

@@ -104,3 +104,26 @@ def s_drops(ser, td):
 
 def s_cross(ser, td):
     return ser.twodrop_solver(td)._keep[1]
+
+
+def test_self_convergence_matches_oracle_golden(ser):
+    """GPU solves at 1/h = 8, 16: the self-convergence errors of eq. (36) equal the
+    oracle's (tests/golden/twodrop_oracle.json) to 1e-6 relative."""
+    import json
+    import os
+
+    from workloads.twodrop import match_nodes, split
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "twodrop_oracle.json")))
+    sols = {}
+    for ih in (8, 16):
+        td = twodrop(ih)
+        u, it, _ = ser.twodrop_solver(td).solve()
+        assert it == g["iterations"][str(ih)]
+        sols[ih] = (td, u.cpu().numpy())
+    idx = match_nodes(sols[8][0], sols[16][0])
+    c, f = split(*sols[8]), split(*sols[16])
+    e = np.concatenate([c[k] - f[k][:, idx[k]] for k in range(2)], axis=1)
+    mag = np.linalg.norm(e, axis=0)
+    assert abs(mag.max() / g["max_err"]["8"] - 1.0) <= 1e-6
+    assert abs(np.sqrt((mag ** 2).mean()) / g["l2_err"]["8"] - 1.0) <= 1e-6
