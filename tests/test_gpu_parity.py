@@ -267,3 +267,14 @@ def test_onsurface_two_sphere_self_block(ser):
             assert rel(u, ur) <= TOL
         if mode & 2:
             assert rel(v, vr) <= TOL
+
+
+def test_delta_power_schedule_parity(ser):
+    """NEXT-4 (delta ~ h^q): the call with h_eff = C h^q (q = 0.8) matches
+    the oracle at the same h_eff, on config 2 at 1/h = 32."""
+    import dataclasses
+
+    blk = config2(inv_h=32)
+    h_eff = blk.h ** 0.8 * (1.0 / 16) ** 0.2
+    b2 = dataclasses.replace(blk, h=h_eff)
+    check_block(ser, b2.take_targets(np.arange(0, b2.M, 7)), localized=True)

@@ -324,3 +324,31 @@ def test_sharp_cutoff_seven(oracle_mod):
     assert abs(1 - float(hp.s_sharp(6.0)[1])) == pytest.approx(2.45e-12, rel=0.01)
     for v in hp.s_sharp(7.0):
         assert abs(1 - float(v)) < 1e-16
+
+
+def test_delta_power_schedule_next4(oracle_mod):
+    """NEXT-4: delta proportional to h^q, q < 1, so that delta/h grows as
+    h -> 0.  The API's h enters only through delta_k = rho_k h (the quadrature
+    weights are inputs), so the schedule is the call with h_eff = C h^q:
+    (i) eval(h_eff, rho) equals eval(h, rho h_eff/h) to rounding, and (ii) with
+    q = 0.8 the SL-translation error still falls at high order (>= 2^3 per halving
+    of h; measured 2^6.4 at these resolutions, where the discretization error, which
+    the growing delta/h suppresses, still dominates the O(delta^5) regularization
+    error) and at 1/h = 32 it is below the q = 1 error (the reason for q < 1)."""
+    q = 0.8
+    blk = config1(f_field=ConstField(F_T), q_field=ZeroField(), inv_h=16, per_class=8)
+    h_eff = blk.h ** q * (1.0 / 16) ** (1 - q)
+    u1, _ = oracle_mod.evaluate(*blk.arrays(), h_eff, blk.rho, mode=1, localized=True)
+    u2, _ = oracle_mod.evaluate(*blk.arrays(), blk.h, tuple(r * h_eff / blk.h for r in blk.rho), mode=1,
+                                localized=True)
+    assert np.abs(u1 - u2).max() <= 1e-15 * np.abs(u1).max() * 10
+    errs = []
+    for inv in (16, 32):
+        b = config1(f_field=ConstField(F_T), q_field=ZeroField(), inv_h=inv, per_class=8)
+        he = b.h ** q * (1.0 / 16) ** (1 - q)
+        u, _ = oracle_mod.evaluate(*b.arrays(), he, b.rho, mode=1, localized=True)
+        errs.append(np.abs(u - sl_translation(F_T, b.tgt_xyz)).max())
+    assert errs[0] / errs[1] > 2 ** 3, errs
+    b = config1(f_field=ConstField(F_T), q_field=ZeroField(), inv_h=32, per_class=8)
+    u, _ = oracle_mod.evaluate(*b.arrays(), b.h, b.rho, mode=1, localized=True)
+    assert errs[1] < np.abs(u - sl_translation(F_T, b.tgt_xyz)).max()
