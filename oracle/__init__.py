@@ -56,6 +56,8 @@ def lib():
                                                  _dp, _dp]
         L.oracle_extrapolate.argtypes = [_dp, ctypes.c_int64, ctypes.c_double, _dp, _dp, ctypes.c_int, _dp]
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_eval_tree.argtypes = common + [_dp, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                                                ctypes.c_int, _dp, _dp, _dp]
         _lib = L
     return _lib
 
@@ -162,3 +164,24 @@ def evaluate_block(block, mode=BOTH, localized=False, nthreads=0):
 
 def eval_deltas_block(block, mode=BOTH, localized=False, nthreads=0):
     return eval_deltas(*block.arrays(), block.h, block.rho, mode=mode, localized=localized, nthreads=nthreads)
+
+
+def evaluate_tree(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho,
+                  leaf_size=2000, degree=6, theta=0.6, mode=BOTH, nthreads=0, stats=False):
+    """NEXT-3: the treecode of PAPER.md Sec. 3.4 for the far part (readings R22-R25 in
+    stokes_er_oracle.c).  Returns (u, v) or (u, v, stats) with stats =
+    (nodes, accepted target-cluster pairs, directly summed target-source pairs)."""
+    arrs, M, N = _inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density)
+    u = np.zeros((3, M)) if mode & SL else None
+    v = np.zeros((3, M)) if mode & DL else None
+    st = np.zeros(3)
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    rc = lib().oracle_eval_tree(*[_p(a) for a in arrs], M, N, float(h), _p(rho), int(mode), int(leaf_size),
+                                int(degree), float(theta), int(nthreads), _p(u), _p(v), _p(st))
+    if rc:
+        raise ValueError(f"oracle_eval_tree: status {rc}")
+    return (u, v, tuple(int(x) for x in st)) if stats else (u, v)
+
+
+def evaluate_tree_block(block, mode=BOTH, nthreads=0, **kw):
+    return evaluate_tree(*block.arrays(), block.h, block.rho, mode=mode, nthreads=nthreads, **kw)

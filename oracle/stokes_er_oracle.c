@@ -126,23 +126,15 @@ static void reg_weights(double r, double delta, double delta1, int sharp, double
   A[2] = s[2] / (r * r * r * r * r);
 }
 
-/* ---- one target: the three regularized sums ------------------------------- */
-static void eval_target(const double* src_xyz, const double* src_normal, const double* src_weight,
-                        const double* f, const double* q, const double y[3], double b,
-                        const double n0[3], const double f0[3], const double q0[3], int64_t N,
-                        const double delta[3], int ndelta, int mode, int localized, int sharp,
-                        double cutoff, double U[3][3], double V[3][3]) {
-  nsum Us[3][3], Vs[3][3], Uf[3], Vf[3];
-  memset(Us, 0, sizeof(Us)); memset(Vs, 0, sizeof(Vs));
-  memset(Uf, 0, sizeof(Uf)); memset(Vf, 0, sizeof(Vf));
-  double x0[3], alpha = 0.0;
-  for (int i = 0; i < 3; ++i) x0[i] = y[i] - b * n0[i];           /* y = x0 + b n0, PAPER.md:107 */
-  for (int i = 0; i < 3; ++i) alpha += f0[i] * n0[i];             /* f(x0).n(x0), PAPER.md:52 */
-  double dmax = delta[0];
-  for (int k = 1; k < ndelta; ++k) dmax = fmax(dmax, delta[k]);
-  const double rc2 = (cutoff * dmax) * (cutoff * dmax);
-
-  for (int64_t s = 0; s < N; ++s) {
+/* ---- one target, sources s0 <= s < s1 (arrays of stride N): accumulate the
+ * pair terms into the per-delta sums Us, Vs (near, or every pair in definition
+ * mode) and the shared far sums Uf, Vf (localized mode, r^2 > rc2). -------- */
+static void accum_pairs(const double* src_xyz, const double* src_normal, const double* src_weight,
+                        const double* f, const double* q, int64_t N, int64_t s0, int64_t s1,
+                        const double y[3], double b, const double n0[3], const double x0[3], double alpha,
+                        const double q0[3], const double delta[3], int ndelta, int mode, int localized,
+                        int sharp, double rc2, nsum Us[3][3], nsum Vs[3][3], nsum Uf[3], nsum Vf[3]) {
+  for (int64_t s = s0; s < s1; ++s) {
     double x[3], m[3], yh[3], xh[3], g[3], dq[3];
     for (int i = 0; i < 3; ++i) {
       x[i] = src_xyz[i * N + s];
@@ -216,6 +208,11 @@ static void eval_target(const double* src_xyz, const double* src_normal, const d
             }
     }
   }
+}
+
+/* per-delta totals: (near + far)/(8 pi), + chi q(x0) for the DL (eqs. (10)-(11)) */
+static void finish_target(double b, const double q0[3], int ndelta, nsum Us[3][3], nsum Vs[3][3],
+                          nsum Uf[3], nsum Vf[3], double U[3][3], double V[3][3]) {
   const double chi = b < 0.0 ? 1.0 : (b > 0.0 ? 0.0 : 0.5);      /* PAPER.md:58 */
   for (int k = 0; k < ndelta; ++k)
     for (int i = 0; i < 3; ++i) {
@@ -225,6 +222,26 @@ static void eval_target(const double* src_xyz, const double* src_normal, const d
       U[k][i] = nval(&u) / (8.0 * ORACLE_PI);
       V[k][i] = nval(&v) / (8.0 * ORACLE_PI) + chi * q0[i];
     }
+}
+
+/* ---- one target: the three regularized sums ------------------------------- */
+static void eval_target(const double* src_xyz, const double* src_normal, const double* src_weight,
+                        const double* f, const double* q, const double y[3], double b,
+                        const double n0[3], const double f0[3], const double q0[3], int64_t N,
+                        const double delta[3], int ndelta, int mode, int localized, int sharp,
+                        double cutoff, double U[3][3], double V[3][3]) {
+  nsum Us[3][3], Vs[3][3], Uf[3], Vf[3];
+  memset(Us, 0, sizeof(Us)); memset(Vs, 0, sizeof(Vs));
+  memset(Uf, 0, sizeof(Uf)); memset(Vf, 0, sizeof(Vf));
+  double x0[3], alpha = 0.0;
+  for (int i = 0; i < 3; ++i) x0[i] = y[i] - b * n0[i];           /* y = x0 + b n0, PAPER.md:107 */
+  for (int i = 0; i < 3; ++i) alpha += f0[i] * n0[i];             /* f(x0).n(x0), PAPER.md:52 */
+  double dmax = delta[0];
+  for (int k = 1; k < ndelta; ++k) dmax = fmax(dmax, delta[k]);
+  const double rc2 = (cutoff * dmax) * (cutoff * dmax);
+  accum_pairs(src_xyz, src_normal, src_weight, f, q, N, 0, N, y, b, n0, x0, alpha, q0, delta, ndelta, mode,
+              localized, sharp, rc2, Us, Vs, Uf, Vf);
+  finish_target(b, q0, ndelta, Us, Vs, Uf, Vf, U, V);
 }
 
 static int check_args(const double* src_xyz, const double* src_normal, const double* src_weight,
@@ -377,4 +394,308 @@ int oracle_max_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/* ===================================================================== NEXT-3
+ * The kernel-independent treecode of PAPER.md Sec. 3.4 (lines 194-233) for the
+ * far part of the localized sums, step by step in the paper's order:
+ *   1. the quadrature points are partitioned into an octree until at most N0
+ *      points remain in a cluster (a leaf)
+ *   2. modified weights (eq. (32) `mod_weights`) at the tensor Chebyshev points
+ *      s_k of each cluster box, for f w and n w (SL) and q n w and n w (DL)
+ *                                                               PAPER.md:215-230
+ *   3. per target, from the root: if the MAC r_c/R <= theta (eq. (28)) holds the
+ *      cluster's interaction is eq. (31) with the unregularized S, T at the s_k;
+ *      otherwise the children are checked; a leaf that fails is summed directly
+ *      with the localized regularization (3 deltas near, shared far) PAPER.md:232
+ * Readings (R22-R25):
+ *   R22 tree: root box = tight box of the points; a cluster with > N0 points and
+ *       a box of non-zero extent is split at its box midpoint in every axis of
+ *       non-zero extent (x_d >= mid_d goes up), points keep their order within
+ *       an octant, empty octants are dropped, children in octant order
+ *       (bit d = upper half in axis d); every box then shrinks to its points'
+ *       tight box.  r_c = half the box diagonal, centre = box midpoint.
+ *   R23 acceptance = MAC AND the box lies beyond the regularization cutoff
+ *       (gap^2 > (c delta_max)^2), so no pair with r <= c delta_max is ever
+ *       approximated; both tests in plain (non-fused) FP64 in a fixed order:
+ *       R^2 = (dx*dx + dy*dy) + dz*dz, accept iff r_c <= theta*sqrt(R^2).
+ *   R24 Chebyshev points of the second kind s_k = c + (w/2) cos(k pi/p), k = 0..p,
+ *       barycentric weights (-1)^k, halved at k = 0 and p; a coordinate within
+ *       1e-14 w of a node takes that node's cardinal value; an axis of zero
+ *       extent interpolates with L_0 = 1.
+ *   R25 far part of a target = sum over accepted clusters of eq. (31) with the
+ *       subtraction structure: SL weights g^fw - alpha g^nw, DL weights
+ *       g^qn_ac - q0_a g^nw_c. */
+typedef struct {
+  double lo[3], hi[3], c[3], rc;
+  int64_t begin, end;  /* tree-order range */
+  int first_child, nchild;
+} tnode;
+
+static void tight_box(const double* xyz, int64_t N, const int64_t* idx, int64_t b, int64_t e, double lo[3],
+                      double hi[3]) {
+  for (int d = 0; d < 3; ++d) { lo[d] = INFINITY; hi[d] = -INFINITY; }
+  for (int64_t j = b; j < e; ++j)
+    for (int d = 0; d < 3; ++d) {
+      const double v = xyz[d * N + idx[j]];
+      if (v < lo[d]) lo[d] = v;
+      if (v > hi[d]) hi[d] = v;
+    }
+}
+
+static void set_geometry(tnode* t) {
+  double s = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    const double w = t->hi[d] - t->lo[d];
+    t->c[d] = 0.5 * (t->lo[d] + t->hi[d]);
+    s = s + w * w;
+  }
+  t->rc = 0.5 * sqrt(s);
+}
+
+/* recursive build (R22); returns the node count or -1 if max_nodes is exceeded */
+static int build_node(const double* xyz, int64_t N, int64_t* idx, int64_t* tmp, tnode* nodes, int self,
+                      int* count, int max_nodes, int64_t N0) {
+  tnode* t = &nodes[self];
+  t->first_child = -1;
+  t->nchild = 0;
+  const int64_t n = t->end - t->begin;
+  int split_axes = 0;
+  for (int d = 0; d < 3; ++d)
+    if (t->hi[d] > t->lo[d]) split_axes |= 1 << d;
+  if (n <= N0 || !split_axes) return 0;
+  double mid[3];
+  for (int d = 0; d < 3; ++d) mid[d] = 0.5 * (t->lo[d] + t->hi[d]);
+  int64_t cnt[8] = {0}, start[8];
+  for (int64_t j = t->begin; j < t->end; ++j) {
+    int o = 0;
+    for (int d = 0; d < 3; ++d)
+      if ((split_axes >> d & 1) && xyz[d * N + idx[j]] >= mid[d]) o |= 1 << d;
+    cnt[o]++;
+  }
+  start[0] = t->begin;
+  for (int o = 1; o < 8; ++o) start[o] = start[o - 1] + cnt[o - 1];
+  int64_t pos[8];
+  memcpy(pos, start, sizeof(pos));
+  for (int64_t j = t->begin; j < t->end; ++j) {
+    int o = 0;
+    for (int d = 0; d < 3; ++d)
+      if ((split_axes >> d & 1) && xyz[d * N + idx[j]] >= mid[d]) o |= 1 << d;
+    tmp[pos[o]++] = idx[j];
+  }
+  memcpy(idx + t->begin, tmp + t->begin, sizeof(int64_t) * (size_t)n);
+  int nc = 0;
+  for (int o = 0; o < 8; ++o) nc += cnt[o] > 0;
+  if (*count + nc > max_nodes) return -1;
+  const int first = *count;
+  *count += nc;
+  t->first_child = first;
+  t->nchild = nc;
+  int k = first;
+  for (int o = 0; o < 8; ++o) {
+    if (!cnt[o]) continue;
+    tnode* ch = &nodes[k];
+    ch->begin = start[o];
+    ch->end = start[o] + cnt[o];
+    tight_box(xyz, N, idx, ch->begin, ch->end, ch->lo, ch->hi);
+    set_geometry(ch);
+    ++k;
+  }
+  for (int j = first; j < first + nc; ++j)
+    if (build_node(xyz, N, idx, tmp, nodes, j, count, max_nodes, N0) < 0) return -1;
+  return 0;
+}
+
+/* 1-D barycentric Lagrange basis at x on the second-kind Chebyshev points of [lo, hi] (R24) */
+static void lagrange_1d(double x, double lo, double hi, int p, double L[]) {
+  const double w = hi - lo;
+  for (int k = 0; k <= p; ++k) L[k] = 0.0;
+  if (!(w > 0.0)) { L[0] = 1.0; return; }
+  const double c = 0.5 * (lo + hi), half = 0.5 * w;
+  double s[64], bw[64];
+  for (int k = 0; k <= p; ++k) {
+    s[k] = c + half * cos(k * ORACLE_PI / p);
+    bw[k] = ((k & 1) ? -1.0 : 1.0) * ((k == 0 || k == p) ? 0.5 : 1.0);
+    if (fabs(x - s[k]) <= 1e-14 * w) { for (int j = 0; j <= p; ++j) L[j] = 0.0; L[k] = 1.0; return; }
+  }
+  double den = 0.0;
+  for (int k = 0; k <= p; ++k) den += bw[k] / (x - s[k]);
+  for (int k = 0; k <= p; ++k) L[k] = (bw[k] / (x - s[k])) / den;
+}
+
+#define TC_CH 15 /* channels: fw (3), nw (3), q_a n_c w (9) */
+
+typedef struct {
+  int p, nnodes;
+  tnode* nodes;
+  int64_t* perm;      /* tree order -> input index */
+  double* mw;         /* [node][(p+1)^3][TC_CH] modified weights */
+} tree_t;
+
+/* Evaluate targets with the treecode.  Inputs as oracle_eval, plus leaf size N0,
+ * degree p and MAC theta.  out_u, out_v: [3][M].  out_stats (may be NULL):
+ * [0] nodes, [1] accepted (target, cluster) pairs, [2] directly summed
+ * (target, source) pairs.  Returns 0, 1 (EINVAL) or 2 (tree too large). */
+int oracle_eval_tree(const double* src_xyz, const double* src_normal, const double* src_weight,
+                     const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                     const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
+                     int mode, int64_t N0, int p, double theta, int nthreads, double* out_u, double* out_v,
+                     double* out_stats) {
+  if (check_args(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, mode)) return 1;
+  if (!(rho[0] > 0.0 && rho[1] > rho[0] && rho[2] > rho[1]) || N0 < 1 || p < 1 || p > 40 || !(theta >= 0.0))
+    return 1;
+  /* 1. tree (R22) */
+  const int max_nodes = (int)(8 * (N / N0) + 4096);
+  tree_t T;
+  T.p = p;
+  T.nodes = (tnode*)calloc((size_t)max_nodes, sizeof(tnode));
+  T.perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)N);
+  int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (size_t)N);
+  for (int64_t j = 0; j < N; ++j) T.perm[j] = j;
+  T.nodes[0].begin = 0;
+  T.nodes[0].end = N;
+  tight_box(src_xyz, N, T.perm, 0, N, T.nodes[0].lo, T.nodes[0].hi);
+  set_geometry(&T.nodes[0]);
+  int count = 1;
+  if (build_node(src_xyz, N, T.perm, tmp, T.nodes, 0, &count, max_nodes, N0) < 0) {
+    free(T.nodes); free(T.perm); free(tmp);
+    return 2;
+  }
+  free(tmp);
+  T.nnodes = count;
+  /* sources in tree order */
+  double *X = (double*)malloc(sizeof(double) * 3 * (size_t)N), *Nr = (double*)malloc(sizeof(double) * 3 * (size_t)N);
+  double *W = (double*)malloc(sizeof(double) * (size_t)N);
+  double *F = (double*)calloc(3 * (size_t)N, sizeof(double)), *Q = (double*)calloc(3 * (size_t)N, sizeof(double));
+  for (int64_t j = 0; j < N; ++j) {
+    const int64_t s = T.perm[j];
+    W[j] = src_weight[s];
+    for (int d = 0; d < 3; ++d) {
+      X[d * N + j] = src_xyz[d * N + s];
+      Nr[d * N + j] = src_normal[d * N + s];
+      if (mode & 1) F[d * N + j] = f[d * N + s];
+      if (mode & 2) Q[d * N + j] = q[d * N + s];
+    }
+  }
+  /* 2. modified weights, eq. (32): g^_k = sum_j L_k1(x_j1) L_k2(x_j2) L_k3(x_j3) g(x_j) */
+  const int P1 = p + 1, NP = P1 * P1 * P1;
+  T.mw = (double*)calloc((size_t)T.nnodes * NP * TC_CH, sizeof(double));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int c = 0; c < T.nnodes; ++c) {
+    const tnode* t = &T.nodes[c];
+    double* G = T.mw + (size_t)c * NP * TC_CH;
+    for (int64_t j = t->begin; j < t->end; ++j) {
+      double L[3][64], g[TC_CH];
+      for (int d = 0; d < 3; ++d) lagrange_1d(X[d * N + j], t->lo[d], t->hi[d], p, L[d]);
+      for (int a = 0; a < 3; ++a) {
+        g[a] = F[a * N + j] * W[j];                  /* f_a w   (SL) */
+        g[3 + a] = Nr[a * N + j] * W[j];             /* n_a w   (SL, DL) */
+        for (int cc = 0; cc < 3; ++cc) g[6 + 3 * a + cc] = Q[a * N + j] * Nr[cc * N + j] * W[j];  /* q_a n_c w */
+      }
+      for (int k1 = 0; k1 < P1; ++k1)
+        for (int k2 = 0; k2 < P1; ++k2)
+          for (int k3 = 0; k3 < P1; ++k3) {
+            const double Lk = L[0][k1] * L[1][k2] * L[2][k3];
+            double* Gk = G + ((size_t)(k1 * P1 + k2) * P1 + k3) * TC_CH;
+            for (int ch = 0; ch < TC_CH; ++ch) Gk[ch] += Lk * g[ch];
+          }
+    }
+  }
+  /* 3. per target traversal */
+  const double delta[3] = {rho[0] * h, rho[1] * h, rho[2] * h};
+  const double rc2 = (ORACLE_CUTOFF * delta[2]) * (ORACLE_CUTOFF * delta[2]);
+  double* ud = (double*)malloc(sizeof(double) * 9 * (size_t)(M > 0 ? M : 1));
+  double* vd = (double*)malloc(sizeof(double) * 9 * (size_t)(M > 0 ? M : 1));
+  double n_acc = 0.0, n_dir = 0.0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : n_acc, n_dir)
+  for (int64_t tg = 0; tg < M; ++tg) {
+    double y[3], n0[3], f0[3], q0[3], x0[3], alpha = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      y[i] = tgt_xyz[i * M + tg];
+      n0[i] = tgt_x0_density[i * M + tg];
+      f0[i] = tgt_x0_density[(3 + i) * M + tg];
+      q0[i] = tgt_x0_density[(6 + i) * M + tg];
+    }
+    const double b = tgt_b[tg];
+    for (int i = 0; i < 3; ++i) x0[i] = y[i] - b * n0[i];
+    for (int i = 0; i < 3; ++i) alpha += f0[i] * n0[i];
+    nsum Us[3][3], Vs[3][3], Uf[3], Vf[3];
+    memset(Us, 0, sizeof(Us)); memset(Vs, 0, sizeof(Vs));
+    memset(Uf, 0, sizeof(Uf)); memset(Vf, 0, sizeof(Vf));
+    int stack[4096], sp = 0;
+    stack[sp++] = 0;
+    while (sp > 0) {
+      const int c = stack[--sp];
+      const tnode* t = &T.nodes[c];
+      /* R23: MAC (eq. 28) and the regularization guard, plain FP64 */
+      const double dx = y[0] - t->c[0], dy = y[1] - t->c[1], dz = y[2] - t->c[2];
+      volatile double R2 = dx * dx;
+      R2 = R2 + dy * dy;
+      R2 = R2 + dz * dz;
+      volatile double g2 = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        double gap = t->lo[d] - y[d];
+        if (y[d] - t->hi[d] > gap) gap = y[d] - t->hi[d];
+        if (gap < 0.0) gap = 0.0;
+        g2 = g2 + gap * gap;
+      }
+      const int accept = (t->rc <= theta * sqrt(R2)) && (g2 > rc2);
+      if (accept) { /* eq. (31): unregularized kernels at the Chebyshev points */
+        n_acc += 1.0;
+        const double* G = T.mw + (size_t)c * NP * TC_CH;
+        double cs[3][64];
+        for (int d = 0; d < 3; ++d)
+          for (int k = 0; k <= p; ++k)
+            cs[d][k] = 0.5 * (t->lo[d] + t->hi[d]) + 0.5 * (t->hi[d] - t->lo[d]) * cos(k * ORACLE_PI / p);
+        for (int k1 = 0; k1 < P1; ++k1)
+          for (int k2 = 0; k2 < P1; ++k2)
+            for (int k3 = 0; k3 < P1; ++k3) {
+              const double* Gk = G + ((size_t)(k1 * P1 + k2) * P1 + k3) * TC_CH;
+              double yh[3] = {y[0] - cs[0][k1], y[1] - cs[1][k2], y[2] - cs[2][k3]};
+              const double r2 = yh[0] * yh[0] + yh[1] * yh[1] + yh[2] * yh[2];
+              const double r = sqrt(r2), r3 = r2 * r, r5 = r3 * r2;
+              if (mode & 1)
+                for (int i = 0; i < 3; ++i)
+                  for (int a = 0; a < 3; ++a) {
+                    const double S = (i == a ? 1.0 / r : 0.0) + yh[i] * yh[a] / r3;   /* eq. (3) */
+                    nadd(&Uf[i], S * (Gk[a] - alpha * Gk[3 + a]));                   /* R25 */
+                  }
+              if (mode & 2)
+                for (int i = 0; i < 3; ++i)
+                  for (int a = 0; a < 3; ++a)
+                    for (int cc = 0; cc < 3; ++cc) {
+                      const double Tt = -6.0 * yh[i] * yh[a] * yh[cc] / r5;             /* eq. (4) */
+                      nadd(&Vf[i], Tt * (Gk[6 + 3 * a + cc] - q0[a] * Gk[3 + cc]));   /* R25 */
+                    }
+            }
+      } else if (t->nchild == 0) { /* leaf: direct sum, localized regularization */
+        n_dir += (double)(t->end - t->begin);
+        accum_pairs(X, Nr, W, F, Q, N, t->begin, t->end, y, b, n0, x0, alpha, q0, delta, 3, mode, 1, 0, rc2,
+                    Us, Vs, Uf, Vf);
+      } else {
+        for (int k = t->nchild - 1; k >= 0; --k) stack[sp++] = t->first_child + k;  /* octant order */
+      }
+    }
+    double U[3][3], V[3][3];
+    finish_target(b, q0, 3, Us, Vs, Uf, Vf, U, V);
+    for (int k = 0; k < 3; ++k)
+      for (int i = 0; i < 3; ++i) {
+        ud[(k * 3 + i) * M + tg] = U[k][i];
+        vd[(k * 3 + i) * M + tg] = V[k][i];
+      }
+  }
+  int rc = 0;
+  if (M > 0 && (mode & 1)) rc = oracle_extrapolate(tgt_b, M, h, rho, ud, 3, out_u);
+  if (!rc && M > 0 && (mode & 2)) rc = oracle_extrapolate(tgt_b, M, h, rho, vd, 3, out_v);
+  if (out_stats) {
+    out_stats[0] = T.nnodes;
+    out_stats[1] = n_acc;
+    out_stats[2] = n_dir;
+  }
+  free(ud); free(vd); free(X); free(Nr); free(W); free(F); free(Q);
+  free(T.nodes); free(T.perm); free(T.mw);
+  return rc;
 }
