@@ -264,6 +264,46 @@ int stokes_er_twodrop_solve(const stokes_er_drop drops[2], const stokes_er_cross
                             const stokes_er_twodrop_params* params, double* out_u, int* out_iters,
                             double* out_res_host, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ===================================================================== NEXT-3
+ * The kernel-independent treecode of PAPER.md Sec. 3.4 (lines 194-233) for the
+ * far part of the localized sums: sources partitioned into an octree with at
+ * most leaf_size (N0) points per leaf (host, stokes_er_tree_build; readings
+ * R22-R25 in DESIGN.md); modified weights (eq. (32)) at the (degree+1)^3
+ * second-kind Chebyshev points of every cluster; per target, a cluster is
+ * approximated by eq. (31) with the unregularized S, T when the MAC
+ * r_c / R <= theta (eq. (28)) holds AND its box lies beyond the cutoff
+ * (gap > STOKES_ER_CUTOFF max delta_k, so no near pair is approximated), else
+ * its children are checked; a leaf that fails is summed directly with the
+ * localized 3-delta regularization.  The extrapolation is as in stokes_er_eval.
+ * The paper's parameter policy (eq. (33)): theta = 0.6,
+ * N0 = 2000 and p = 6 at h = 1/64, N0 doubling and p + 2 per halving of h.
+ *
+ * Plan: HOST memory of stokes_er_tree_plan_bytes(N, params) bytes, written by
+ * stokes_er_tree_build from HOST node positions [3][N]; reusable for every
+ * evaluation on the same nodes (densities may change).  stokes_er_eval_tree
+ * copies it to the device workspace (stokes_er_tree_workspace_bytes) on
+ * `stream`; other arguments and errors as stokes_er_eval.  EINVAL also for a
+ * plan built for another N, degree > 16, or a tree over 8 N/N0 + 4096 nodes or
+ * 63 levels.
+ */
+typedef struct {
+  int leaf_size;          /* N0: at most N0 points per leaf                          */
+  int degree;             /* p: Chebyshev degree per axis, 1..16                     */
+  double theta;           /* MAC parameter (0: never approximate = direct sum)       */
+} stokes_er_tree_params;
+
+size_t stokes_er_tree_plan_bytes(int64_t N, const stokes_er_tree_params* params);
+int stokes_er_tree_build(const double* src_xyz_host, int64_t N, const stokes_er_tree_params* params, void* plan,
+                         size_t plan_bytes);
+int stokes_er_tree_info(const void* plan, int64_t N, int64_t* out_nodes, int64_t* out_depth);
+size_t stokes_er_tree_workspace_bytes(int64_t M, int64_t N, int mode, const stokes_er_tree_params* params,
+                                      const void* plan);
+int stokes_er_eval_tree(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
+                        const double* q, const double* tgt_xyz, const double* tgt_b, const double* tgt_x0_density,
+                        int64_t M, int64_t N, double h, const double rho[3], int mode,
+                        const stokes_er_tree_params* params, const void* plan, double* out_u, double* out_v,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
 const char* stokes_er_status_string(int status);
 int stokes_er_abi_version(void);
 

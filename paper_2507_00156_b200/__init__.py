@@ -282,3 +282,68 @@ def twodrop_solver(td, device="cuda", max_iter=100, stream=None):
         import numpy as np
         cross.append(dict(b=dev(c.b), x0d=dev(np.ascontiguousarray(np.concatenate([c.n0, c.f0], axis=0)))))
     return TwoDropSolver(drops, cross, td.h, td.rho, td.delta_self, 1.0, td.tol, max_iter, stream)
+
+
+class TreePlan:
+    """NEXT-3 octree over HOST node positions (stokes_er_tree_build, Sec. 3.4).
+    leaf_size = N0, degree = p, theta = MAC parameter (eq. (28))."""
+
+    def __init__(self, src_xyz_host, leaf_size=2000, degree=6, theta=0.6):
+        import numpy as np
+
+        L = _lib.load()
+        x = np.ascontiguousarray(src_xyz_host, dtype=np.float64)
+        if x.ndim != 2 or x.shape[0] != 3:
+            raise ValueError("src_xyz_host: expected (3, N) float64")
+        self.N = int(x.shape[1])
+        self.params = _lib.TreeParams(int(leaf_size), int(degree), float(theta))
+        nbytes = int(L.stokes_er_tree_plan_bytes(self.N, ctypes.byref(self.params)))
+        if nbytes == 0:
+            raise ValueError("stokes_er_tree_plan_bytes: invalid parameters")
+        self.buf = np.zeros(nbytes, dtype=np.uint8)
+        _lib.check("stokes_er_tree_build", L.stokes_er_tree_build(
+            x.ctypes.data_as(ctypes.c_void_p), self.N, ctypes.byref(self.params),
+            self.buf.ctypes.data_as(ctypes.c_void_p), nbytes))
+        n, d = ctypes.c_int64(0), ctypes.c_int64(0)
+        _lib.check("stokes_er_tree_info", L.stokes_er_tree_info(self.ptr(), self.N, ctypes.byref(n), ctypes.byref(d)))
+        self.nodes, self.depth = int(n.value), int(d.value)
+
+    def ptr(self):
+        return self.buf.ctypes.data_as(ctypes.c_void_p)
+
+
+def evaluate_tree(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho, plan: TreePlan,
+                  mode=BOTH, out_u=None, out_v=None, workspace=None, stream=None):
+    """stokes_er_eval_tree on device tensors with a TreePlan over the same nodes."""
+    torch = _torch()
+    M, N = _shapes(src_xyz, tgt_b)
+    dev = src_xyz.device
+    for name, t, shp in (("src_xyz", src_xyz, (3, N)), ("src_normal", src_normal, (3, N)),
+                         ("src_weight", src_weight, (N,)), ("tgt_xyz", tgt_xyz, (3, M)), ("tgt_b", tgt_b, (M,)),
+                         ("tgt_x0_density", tgt_x0_density, (9, M))):
+        _check_dev(name, t, shp)
+    _check_dev("f", f if mode & SL else None, (3, N))
+    _check_dev("q", q if mode & DL else None, (3, N))
+    if plan.N != N:
+        raise ValueError("plan built for another node count")
+    L = _lib.load()
+    if mode & SL and out_u is None:
+        out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    if mode & DL and out_v is None:
+        out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+    if workspace is None:
+        nbytes = int(L.stokes_er_tree_workspace_bytes(M, N, mode, ctypes.byref(plan.params), plan.ptr()))
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    st = L.stokes_er_eval_tree(_ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
+                               _ptr(q if mode & DL else None), _ptr(tgt_xyz), _ptr(tgt_b), _ptr(tgt_x0_density), M,
+                               N, float(h), _lib.rho_arg(rho), int(mode), ctypes.byref(plan.params), plan.ptr(),
+                               _ptr(out_u if mode & SL else None), _ptr(out_v if mode & DL else None),
+                               _ptr(workspace), int(workspace.numel()), _stream_handle(stream))
+    _lib.check("stokes_er_eval_tree", st)
+    return (out_u if mode & SL else None), (out_v if mode & DL else None)
+
+
+def evaluate_tree_block(block, plan=None, mode=BOTH, device="cuda", leaf_size=2000, degree=6, theta=0.6, **kw):
+    if plan is None:
+        plan = TreePlan(block.src_xyz, leaf_size, degree, theta)
+    return evaluate_tree(*to_device(block, device), block.h, block.rho, plan, mode=mode, **kw)

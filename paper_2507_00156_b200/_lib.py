@@ -45,10 +45,16 @@ class TwoDropParams(ctypes.Structure):
                 ("mu0", ctypes.c_double), ("tol", ctypes.c_double), ("max_iter", ctypes.c_int)]
 
 
+class TreeParams(ctypes.Structure):
+    _fields_ = [("leaf_size", ctypes.c_int), ("degree", ctypes.c_int), ("theta", ctypes.c_double)]
+
+
 EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_er_eval", "stokes_er_eval_ex", "stokes_er_host_workspace_bytes",
            "stokes_er_eval_host", "stokes_er_eval_deltas", "stokes_er_eval_onsurface", "stokes_er_extrapolate", "stokes_er_launch_count",
            "stokes_er_status_string", "stokes_er_abi_version", "stokes_er_twodrop_workspace_bytes",
-           "stokes_er_twodrop_setup", "stokes_er_twodrop_rhs", "stokes_er_twodrop_apply", "stokes_er_twodrop_solve"]
+           "stokes_er_twodrop_setup", "stokes_er_twodrop_rhs", "stokes_er_twodrop_apply", "stokes_er_twodrop_solve",
+           "stokes_er_tree_plan_bytes", "stokes_er_tree_build", "stokes_er_tree_info", "stokes_er_tree_workspace_bytes",
+           "stokes_er_eval_tree"]
 
 _lib = None
 
@@ -101,6 +107,18 @@ def load():
     L.stokes_er_twodrop_solve.argtypes = td + [_dp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                                _dp, ctypes.c_size_t, _dp]
     L.stokes_er_twodrop_solve.restype = ctypes.c_int
+    tp = ctypes.POINTER(TreeParams)
+    L.stokes_er_tree_plan_bytes.argtypes = [_i64, tp]
+    L.stokes_er_tree_plan_bytes.restype = ctypes.c_size_t
+    L.stokes_er_tree_build.argtypes = [_dp, _i64, tp, _dp, ctypes.c_size_t]
+    L.stokes_er_tree_build.restype = ctypes.c_int
+    L.stokes_er_tree_info.argtypes = [_dp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+    L.stokes_er_tree_info.restype = ctypes.c_int
+    L.stokes_er_tree_workspace_bytes.argtypes = [_i64, _i64, ctypes.c_int, tp, _dp]
+    L.stokes_er_tree_workspace_bytes.restype = ctypes.c_size_t
+    L.stokes_er_eval_tree.argtypes = [_dp] * 8 + [_i64, _i64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                                                  ctypes.c_int, tp, _dp, _dp, _dp, _dp, ctypes.c_size_t, _dp]
+    L.stokes_er_eval_tree.restype = ctypes.c_int
     _lib = L
     return L
 

@@ -6,6 +6,7 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "treecode.cuh"
 
 namespace ser {
 
@@ -367,6 +368,129 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
 }
 
 
+// NEXT-3: the treecode evaluation (treecode.cuh).  Same pipeline as run_eval
+// with the sources in tree order (the plan's permutation), the far part from
+// tree_far_kernel and the near pairs from the near units.
+struct TreeWs {
+  size_t off_nodes, off_perm, off_G, total;
+};
+TreeWs tree_ws_layout(const Plan& P, int nnodes, int64_t N, int p) {
+  TreeWs w;
+  size_t off = align_up(P.total);
+  w.off_nodes = off;
+  off = align_up(off + (size_t)nnodes * sizeof(TreeNode));
+  w.off_perm = off;
+  off = align_up(off + (size_t)N * sizeof(int32_t));
+  w.off_G = off;
+  off = align_up(off + (size_t)nnodes * (p + 1) * (p + 1) * (p + 1) * kTreeCh * sizeof(double));
+  w.total = off;
+  return w;
+}
+
+template <int MODE>
+int run_eval_tree(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
+                  const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
+                  const double* rho, const stokes_er_tree_params* tp, const TreePlanHeader* hdr,
+                  const char* plan, double* out_u, double* out_v, char* ws, const Plan& P, const TreeWs& W,
+                  cudaStream_t s) {
+  long long* box = reinterpret_cast<long long*>(ws + P.off_box);
+  uint32_t* tkin = reinterpret_cast<uint32_t*>(ws + P.off_tkin);
+  uint32_t* tkout = reinterpret_cast<uint32_t*>(ws + P.off_tkout);
+  int32_t* tvin = reinterpret_cast<int32_t*>(ws + P.off_tvin);
+  int32_t* tvout = reinterpret_cast<int32_t*>(ws + P.off_tvout);
+  double* src = reinterpret_cast<double*>(ws + P.off_src);
+  double* srcbox = reinterpret_cast<double*>(ws + P.off_srcbox);
+  double* tgt = reinterpret_cast<double*>(ws + P.off_tgt);
+  int32_t* orig = reinterpret_cast<int32_t*>(ws + P.off_orig);
+  double* partial = reinterpret_cast<double*>(ws + P.off_partial);
+  double* near_out = reinterpret_cast<double*>(ws + P.off_near);
+  int* counter = reinterpret_cast<int*>(ws + P.off_counter);
+  TreeNode* nodes = reinterpret_cast<TreeNode*>(ws + W.off_nodes);
+  int32_t* perm = reinterpret_cast<int32_t*>(ws + W.off_perm);
+  double* G = reinterpret_cast<double*>(ws + W.off_G);
+  const int nn = hdr->nnodes, p = tp->degree;
+
+  if (cudaMemcpyAsync(nodes, plan + hdr->off_nodes, (size_t)nn * sizeof(TreeNode), cudaMemcpyHostToDevice, s) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(perm, plan + hdr->off_perm, (size_t)N * sizeof(int32_t), cudaMemcpyHostToDevice, s) !=
+          cudaSuccess)
+    return STOKES_ER_ECUDA;
+  if (cudaMemsetAsync(box, 0x7f, 3 * sizeof(long long), s) != cudaSuccess ||
+      cudaMemsetAsync(box + 3, 0x80, 3 * sizeof(long long), s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  bbox_kernel<<<static_cast<int>(std::min<int64_t>(2 * 148, ceil_div(N + M, 256))), 256, 0, s>>>(sx, N, ty, M, box);
+  morton_kernel<<<ceil_div(M, 256), 256, 0, s>>>(ty, M, box, tkin, tvin);
+  size_t cb = P.cub_bytes;
+  if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, tkin, tkout, tvin, tvout, (int)M, 0, 30, s) !=
+      cudaSuccess)
+    return STOKES_ER_ECUDA;
+  pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, perm, src, srcbox);
+  Delta3 r3{{rho[0], rho[1], rho[2]}};
+  pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, false, tgt, orig);
+  tree_weights_kernel<MODE><<<nn, 256, 0, s>>>(nodes, src, p, G);
+  if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
+  const double dmax = rho[2] * h;
+  const double rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  TreeFarParams tfp;
+  tfp.nodes = nodes;
+  tfp.G = G;
+  tfp.src = src;
+  tfp.tgt = tgt;
+  tfp.partial = partial;
+  tfp.counter = counter;
+  tfp.Mpad = P.Mpad;
+  tfp.n_groups = static_cast<int>(P.Mpad / 32);
+  tfp.p = p;
+  tfp.theta = tp->theta;
+  tfp.rc2 = rc2;
+  {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tree_far_kernel<MODE>, kTreeWarps * 32, 0);
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(tfp.n_groups, kTreeWarps), (int64_t)sms * std::max(occ, 1))));
+    tree_far_kernel<MODE><<<grid, kTreeWarps * 32, 0, s>>>(tfp);
+  }
+  NearParams np;
+  np.src = src;
+  np.src_box = srcbox;
+  np.tgt = tgt;
+  np.near_out = near_out;
+  np.counter = counter + 1;
+  np.phases = P.near_phases;
+  np.n_units = static_cast<int>((P.Mpad / 32) * P.near_phases);
+  np.Mpad = P.Mpad;
+  np.Npad = P.Npad;
+  np.rc2 = rc2;
+  np.rc2_box = rc2 * (1.0 + 1e-9);
+  np.r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
+  for (int k = 0; k < 3; ++k) np.inv_delta[k] = 1.0 / (rho[k] * h);
+  {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_kernel<MODE, false>, kNearWarps * 32, 0);
+    const int ngrid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(occ, 1))));
+    near_kernel<MODE, false><<<ngrid, kNearWarps * 32, 0, s>>>(np);
+  }
+  finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad, 1, 32,
+                                                          P.near_phases, out_u, out_v);
+  return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+bool tree_params_ok(const stokes_er_tree_params* tp) {
+  return tp && tp->leaf_size >= 1 && tp->degree >= 1 && tp->degree <= kTreeMaxDegree && std::isfinite(tp->theta) &&
+         tp->theta >= 0.0;
+}
+
+const TreePlanHeader* tree_header(const void* plan, int64_t N) {
+  if (!plan) return nullptr;
+  const TreePlanHeader* h = static_cast<const TreePlanHeader*>(plan);
+  if (h->magic != kTreeMagic || h->N != N || h->nnodes < 1) return nullptr;
+  return h;
+}
+
 size_t host_stage_bytes(int64_t M, int64_t N) {
   return align_up(13 * N * sizeof(double)) + align_up(13 * M * sizeof(double)) + align_up(6 * M * sizeof(double)) +
          4 * kAlign;
@@ -556,5 +680,94 @@ const char* stokes_er_status_string(int status) {
 }
 
 int stokes_er_abi_version(void) { return STOKES_ER_ABI_VERSION; }
+
+
+size_t stokes_er_tree_plan_bytes(int64_t N, const stokes_er_tree_params* params) {
+  if (N < 1 || N > INT32_MAX || !tree_params_ok(params)) return 0;
+  return tree_plan_bytes(N, params->leaf_size);
+}
+
+int stokes_er_tree_build(const double* src_xyz_host, int64_t N, const stokes_er_tree_params* params, void* plan,
+                         size_t plan_bytes) {
+  if (!src_xyz_host || N < 1 || N > INT32_MAX || !tree_params_ok(params) || !plan) return STOKES_ER_EINVAL;
+  if (plan_bytes < tree_plan_bytes(N, params->leaf_size)) return STOKES_ER_EWORKSPACE;
+  TreeBuilder b;
+  b.x = src_xyz_host;
+  b.N = N;
+  b.N0 = params->leaf_size;
+  b.max_nodes = tree_max_nodes(N, params->leaf_size);
+  b.idx.resize(N);
+  b.tmp.resize(N);
+  for (int64_t j = 0; j < N; ++j) b.idx[j] = static_cast<int32_t>(j);
+  TreeNode root{};
+  root.begin = 0;
+  root.end = static_cast<int32_t>(N);
+  b.tight_box(root);
+  for (int d = 0; d < 3; ++d)
+    if (!std::isfinite(root.lo[d]) || !std::isfinite(root.hi[d])) return STOKES_ER_EINVAL;
+  b.nodes.reserve(1024);
+  b.nodes.push_back(root);
+  if (!b.split(0, 0)) return STOKES_ER_EINVAL;  // too many nodes or too deep
+  char* out = static_cast<char*>(plan);
+  TreePlanHeader hdr{};
+  hdr.magic = kTreeMagic;
+  hdr.N = N;
+  hdr.nnodes = static_cast<int32_t>(b.nodes.size());
+  hdr.max_nodes = static_cast<int32_t>(b.max_nodes);
+  hdr.leaf_size = params->leaf_size;
+  hdr.depth = b.depth;
+  hdr.off_nodes = 64;
+  hdr.off_perm = 64 + (int64_t)b.nodes.size() * (int64_t)sizeof(TreeNode);
+  std::memcpy(out, &hdr, sizeof(hdr));
+  std::memcpy(out + hdr.off_nodes, b.nodes.data(), b.nodes.size() * sizeof(TreeNode));
+  std::memcpy(out + hdr.off_perm, b.idx.data(), (size_t)N * sizeof(int32_t));
+  return STOKES_ER_OK;
+}
+
+int stokes_er_tree_info(const void* plan, int64_t N, int64_t* out_nodes, int64_t* out_depth) {
+  const TreePlanHeader* h = tree_header(plan, N);
+  if (!h) return STOKES_ER_EINVAL;
+  if (out_nodes) *out_nodes = h->nnodes;
+  if (out_depth) *out_depth = h->depth;
+  return STOKES_ER_OK;
+}
+
+size_t stokes_er_tree_workspace_bytes(int64_t M, int64_t N, int mode, const stokes_er_tree_params* params,
+                                      const void* plan) {
+  if (M < 0 || N < 1 || mode < 1 || mode > 3 || !tree_params_ok(params)) return 0;
+  const TreePlanHeader* h = tree_header(plan, N);
+  if (!h) return 0;
+  const Plan P = make_plan(M, N, mode, 1, 0);
+  return tree_ws_layout(P, h->nnodes, N, params->degree).total;
+}
+
+int stokes_er_eval_tree(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
+                        const double* q, const double* tgt_xyz, const double* tgt_b, const double* tgt_x0_density,
+                        int64_t M, int64_t N, double h, const double rho[3], int mode,
+                        const stokes_er_tree_params* params, const void* plan, double* out_u, double* out_v,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  int st = validate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode);
+  if (st) return st;
+  if (!tree_params_ok(params)) return STOKES_ER_EINVAL;
+  const TreePlanHeader* hdr = tree_header(plan, N);
+  if (!hdr) return STOKES_ER_EINVAL;
+  if (M == 0) return STOKES_ER_OK;
+  if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
+  if ((st = check_arch())) return st;
+  const Plan P = make_plan(M, N, mode, 1, 0);
+  const TreeWs W = tree_ws_layout(P, hdr->nnodes, N, params->degree);
+  if (!workspace || workspace_bytes < W.total) return STOKES_ER_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  const char* pl = static_cast<const char*>(plan);
+  switch (mode) {
+    case 1: return run_eval_tree<1>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
+                                    rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
+    case 2: return run_eval_tree<2>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
+                                    rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
+    default: return run_eval_tree<3>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N,
+                                     h, rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
+  }
+}
 
 }  // extern "C"
