@@ -372,7 +372,7 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
 // with the sources in tree order (the plan's permutation), the far part from
 // tree_far_kernel and the near pairs from the near units.
 struct TreeWs {
-  size_t off_nodes, off_perm, off_G, total;
+  size_t off_nodes, off_perm, off_G, off_sched, total;
 };
 TreeWs tree_ws_layout(const Plan& P, int nnodes, int64_t N, int p) {
   TreeWs w;
@@ -383,6 +383,8 @@ TreeWs tree_ws_layout(const Plan& P, int nnodes, int64_t N, int p) {
   off = align_up(off + (size_t)N * sizeof(int32_t));
   w.off_G = off;
   off = align_up(off + (size_t)nnodes * (p + 1) * (p + 1) * (p + 1) * kTreeCh * sizeof(double));
+  w.off_sched = off;
+  off = align_up(off + (size_t)nnodes * sizeof(int));
   w.total = off;
   return w;
 }
@@ -427,7 +429,32 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, perm, src, srcbox);
   Delta3 r3{{rho[0], rho[1], rho[2]}};
   pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, false, tgt, orig);
-  tree_weights_kernel<MODE><<<nn, 256, 0, s>>>(nodes, src, p, G);
+  {  // modified weights: leaves from their sources, then internal nodes level by level (M2M)
+    const TreeNode* hn = reinterpret_cast<const TreeNode*>(plan + hdr->off_nodes);
+    std::vector<int> sched;
+    std::vector<int> level_start;
+    for (int i = 0; i < nn; ++i)
+      if (hn[i].nchild == 0) sched.push_back(i);
+    const int n_leaves = static_cast<int>(sched.size());
+    for (int lv = hdr->depth; lv >= 0; --lv) {
+      level_start.push_back(static_cast<int>(sched.size()));
+      for (int i = 0; i < nn; ++i)
+        if (hn[i].nchild > 0 && hn[i].level == lv) sched.push_back(i);
+    }
+    level_start.push_back(static_cast<int>(sched.size()));
+    int* ids = reinterpret_cast<int*>(ws + W.off_sched);
+    if (cudaMemcpyAsync(ids, sched.data(), sched.size() * sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return STOKES_ER_ECUDA;
+    tree_p2m_kernel<MODE><<<n_leaves, 256, 0, s>>>(nodes, ids, src, p, G);
+    const int m2m_smem = 2 * (p + 1) * (p + 1) * (p + 1) * static_cast<int>(sizeof(double));
+    if (cudaFuncSetAttribute(tree_m2m_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, m2m_smem) !=
+        cudaSuccess)
+      return STOKES_ER_ECUDA;
+    for (size_t l = 0; l + 1 < level_start.size(); ++l) {
+      const int a = level_start[l], b = level_start[l + 1];
+      if (b > a) tree_m2m_kernel<MODE><<<b - a, 256, m2m_smem, s>>>(nodes, ids + a, p, G);
+    }
+  }
   if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
   const double dmax = rho[2] * h;
   const double rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);

@@ -4,7 +4,9 @@
 //   host   : octree over the sources (stokes_er_tree_build, readings R22)
 //   KW     : modified weights, eq. (32), at the (p+1)^3 second-kind Chebyshev
 //            points of every cluster box (R24), 15 channels: f w, n w (SL) and
-//            q_a n_c w (DL; the DL's n w channel is the SL's)  -- tree_weights_kernel
+//            q_a n_c w (DL; the DL n w channel is the SL one): leaves from their
+//            sources (tree_p2m_kernel), internal nodes from their children level by
+//            level (tree_m2m_kernel, separable; exact for degree-p interpolants)
 //   KT     : far part per target: a warp of 32 Morton-consecutive targets walks
 //            the tree depth-first with a warp-uniform stack of (cluster, lane
 //            mask); each lane decides MAC + regularization guard for its own
@@ -31,7 +33,7 @@ constexpr uint64_t kTreeMagic = 0x53455254524545ULL;  // "SERTREE"
 
 struct TreeNode {  // POD, identical on host and device
   double lo[3], hi[3], c[3], rc;
-  int32_t begin, end, first_child, nchild;
+  int32_t begin, end, first_child, nchild, level, pad;
 };
 
 struct TreePlanHeader {
@@ -108,6 +110,7 @@ struct TreeBuilder {
     for (int o = 0; o < 8; ++o) {
       if (!cnt[o]) continue;
       TreeNode ch{};
+      ch.level = level + 1;
       ch.begin = static_cast<int32_t>(start[o]);
       ch.end = static_cast<int32_t>(start[o] + cnt[o]);
       tight_box(ch);
@@ -146,20 +149,22 @@ __device__ __forceinline__ void tree_lagrange(double x, double lo, double hi, in
   for (int k = 0; k <= p; ++k) L[k] *= inv;
 }
 
-// KW: modified weights of every cluster (eq. (32)): G[node][k][ch] = sum_j L_k(x_j) g_ch(x_j),
-// sources j of the node in tree order.  One CTA per node; threads own proxy points.
+// KW1 (leaves): modified weights, eq. (32): G[node][k][ch] = sum_j L_k(x_j) g_ch(x_j),
+// sources j of the leaf in tree order.  One CTA per leaf (ids[blockIdx.x]);
+// threads own proxy points.
 constexpr int kTwChunk = 32;
 template <int MODE>
-__global__ void __launch_bounds__(256) tree_weights_kernel(const TreeNode* __restrict__ nodes,
-                                                           const double* __restrict__ src, int p,
-                                                           double* __restrict__ G) {
+__global__ void __launch_bounds__(256) tree_p2m_kernel(const TreeNode* __restrict__ nodes,
+                                                       const int* __restrict__ ids, const double* __restrict__ src,
+                                                       int p, double* __restrict__ G) {
   __shared__ double sL[kTwChunk][3][kTreeMaxDegree + 1];
   __shared__ double sg[kTwChunk][kTreeCh];
   __shared__ double cosk[kTreeMaxDegree + 1];
-  const TreeNode nd = nodes[blockIdx.x];
+  const int node = ids[blockIdx.x];
+  const TreeNode nd = nodes[node];
   const int P1 = p + 1, NP = P1 * P1 * P1;
   if (threadIdx.x <= p) cosk[threadIdx.x] = cos(threadIdx.x * kPi / p);
-  double* Gn = G + (size_t)blockIdx.x * NP * kTreeCh;
+  double* Gn = G + (size_t)node * NP * kTreeCh;
   for (int k0 = 0; k0 < NP; k0 += blockDim.x) {
     const int k = k0 + threadIdx.x;
     const int k1 = k / (P1 * P1), k2 = (k / P1) % P1, k3 = k % P1;
@@ -189,6 +194,66 @@ __global__ void __launch_bounds__(256) tree_weights_kernel(const TreeNode* __res
     if (k < NP)
 #pragma unroll
       for (int c = 0; c < kTreeCh; ++c) Gn[(size_t)k * kTreeCh + c] = acc[c];
+  }
+}
+
+// KW2 (internal nodes, one level at a time from the deepest): the parent's
+// modified weights from its children's, G^P_k = sum_C sum_k' L^P_k1(s^C_k1')
+// L^P_k2(s^C_k2') L^P_k3(s^C_k3') G^C_k'.  Exact in exact arithmetic: each
+// L^P_k is a polynomial of degree p per axis, reproduced by the child's
+// degree-p interpolation, so this equals eq. (32) summed over the parent's
+// sources (what the oracle computes) up to rounding.
+template <int MODE>
+__global__ void __launch_bounds__(256) tree_m2m_kernel(const TreeNode* __restrict__ nodes,
+                                                       const int* __restrict__ ids, int p, double* __restrict__ G) {
+  // separable form: for each child and channel, three 1-D contractions through
+  // SMEM (B0 -> B1 -> B0 -> += G^P), 3 (p+1)^4 FMAs instead of (p+1)^6
+  __shared__ double A[3][kTreeMaxDegree + 1][kTreeMaxDegree + 1];  // A[d][k'][k] = L^P_k(s^C_k',d)
+  __shared__ double cosk[kTreeMaxDegree + 1];
+  extern __shared__ double dyn[];
+  const int node = ids[blockIdx.x];
+  const TreeNode P = nodes[node];
+  const int P1 = p + 1, NP = P1 * P1 * P1;
+  double* B0 = dyn;
+  double* B1 = dyn + NP;
+  if (threadIdx.x <= p) cosk[threadIdx.x] = cos(threadIdx.x * kPi / p);
+  double* GP = G + (size_t)node * NP * kTreeCh;
+  for (int ci = 0; ci < P.nchild; ++ci) {
+    const int child = P.first_child + ci;
+    const TreeNode C = nodes[child];
+    const double* GC = G + (size_t)child * NP * kTreeCh;
+    __syncthreads();  // previous child's A consumed (and cosk written)
+    if (threadIdx.x < 3 * P1) {
+      const int d = threadIdx.x / P1, kp = threadIdx.x % P1;
+      const double sc = C.c[d] + 0.5 * (C.hi[d] - C.lo[d]) * cosk[kp];
+      tree_lagrange(sc, P.lo[d], P.hi[d], p, cosk, A[d][kp]);
+    }
+    for (int c = 0; c < kTreeCh; ++c) {
+      __syncthreads();
+      for (int k = threadIdx.x; k < NP; k += blockDim.x) B0[k] = GC[(size_t)k * kTreeCh + c];
+      __syncthreads();
+      for (int k = threadIdx.x; k < NP; k += blockDim.x) {  // axis 0: [a][b][cc] -> [k1][b][cc]
+        const int k1 = k / (P1 * P1), r = k % (P1 * P1);
+        double v = 0.0;
+        for (int a2 = 0; a2 < P1; ++a2) v = fma(A[0][a2][k1], B0[a2 * P1 * P1 + r], v);
+        B1[k] = v;
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < NP; k += blockDim.x) {  // axis 1: [k1][b][cc] -> [k1][k2][cc]
+        const int k1 = k / (P1 * P1), k2 = (k / P1) % P1, cc = k % P1;
+        double v = 0.0;
+        for (int b2 = 0; b2 < P1; ++b2) v = fma(A[1][b2][k2], B1[(k1 * P1 + b2) * P1 + cc], v);
+        B0[k] = v;
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < NP; k += blockDim.x) {  // axis 2, accumulate into the parent
+        const int base = k - k % P1, k3 = k % P1;
+        double v = 0.0;
+        for (int c2 = 0; c2 < P1; ++c2) v = fma(A[2][c2][k3], B0[base + c2], v);
+        double* out = GP + (size_t)k * kTreeCh + c;
+        *out = (ci == 0) ? v : *out + v;
+      }
+    }
   }
 }
 
