@@ -425,7 +425,10 @@ int oracle_max_threads(void) {
  *       extent interpolates with L_0 = 1.
  *   R25 far part of a target = sum over accepted clusters of eq. (31) with the
  *       subtraction structure: SL weights g^fw - alpha g^nw, DL weights
- *       g^qn_ac - q0_a g^nw_c. */
+ *       g^qn_ac - q0_a g^nw_c.
+ *   R26 an accepted cluster with at most (p+1)^3 points is summed directly
+ *       (its far pairs exactly) instead of through its (p+1)^3 Chebyshev points,
+ *       which would cost more and be less accurate; the paper is silent. */
 typedef struct {
   double lo[3], hi[3], c[3], rc;
   int64_t begin, end;  /* tree-order range */
@@ -643,7 +646,7 @@ int oracle_eval_tree(const double* src_xyz, const double* src_normal, const doub
         g2 = g2 + gap * gap;
       }
       const int accept = (t->rc <= theta * sqrt(R2)) && (g2 > rc2);
-      if (accept) { /* eq. (31): unregularized kernels at the Chebyshev points */
+      if (accept && t->end - t->begin > NP) { /* eq. (31): unregularized kernels at the Chebyshev points */
         n_acc += 1.0;
         const double* G = T.mw + (size_t)c * NP * TC_CH;
         double cs[3][64];
@@ -671,7 +674,9 @@ int oracle_eval_tree(const double* src_xyz, const double* src_normal, const doub
                       nadd(&Vf[i], Tt * (Gk[6 + 3 * a + cc] - q0[a] * Gk[3 + cc]));   /* R25 */
                     }
             }
-      } else if (t->nchild == 0) { /* leaf: direct sum, localized regularization */
+      } else if (accept || t->nchild == 0) {
+        /* a leaf that fails, or an accepted cluster with no more points than
+         * Chebyshev points (R26): direct sum, localized regularization */
         n_dir += (double)(t->end - t->begin);
         accum_pairs(X, Nr, W, F, Q, N, t->begin, t->end, y, b, n0, x0, alpha, q0, delta, 3, mode, 1, 0, rc2,
                     Us, Vs, Uf, Vf);

@@ -12,8 +12,9 @@
 //            mask); each lane decides MAC + regularization guard for its own
 //            target (R23, plain FP64 in the oracle's order, so the decisions are
 //            the oracle's); accepted lanes add eq. (31) at the cluster's
-//            Chebyshev points, lanes that reject a leaf add its far pairs
-//            directly (near pairs masked)                       -- tree_far_kernel
+//            Chebyshev points (or, R26, its far pairs directly when it has at most
+//            (p+1)^3 points), lanes that reject a leaf add its far pairs directly
+//            (near pairs masked)                                -- tree_far_kernel
 //   K3     : the near pairs, all in directly summed leaves (R23), by the near
 //            units of the direct path over the tree-ordered sources
 //   K2     : finalize (far partial + near phases, 1/(8pi), -6, chi q0)
@@ -326,8 +327,12 @@ __global__ void __launch_bounds__(kTreeWarps * 32) tree_far_kernel(const TreeFar
         }
         acc_lane = (nd.rc <= __dmul_rn(p.theta, __dsqrt_rn(R2))) && (g2 > p.rc2);
       }
-      const unsigned amask = __ballot_sync(0xffffffffu, acc_lane);
-      const unsigned rmask = mask & ~amask;
+      const unsigned accm = __ballot_sync(0xffffffffu, acc_lane);
+      // R26: an accepted cluster with at most (p+1)^3 points is summed directly
+      const bool small = nd.end - nd.begin <= NP;
+      const unsigned amask = small ? 0u : accm;                          // approximated (eq. 31)
+      const unsigned dmask = (small ? accm : 0u) | (nd.nchild == 0 ? mask & ~accm : 0u);  // direct
+      const unsigned rmask = nd.nchild == 0 ? 0u : mask & ~accm;         // recurse into the children
       if (amask) {  // eq. (31) at the cluster's Chebyshev points (unregularized S, T)
         const bool on = amask >> lane & 1;
         const double* Gn = p.G + (size_t)ni * NP * kTreeCh;
@@ -344,19 +349,24 @@ __global__ void __launch_bounds__(kTreeWarps * 32) tree_far_kernel(const TreeFar
             for (int c = 0; c < kTreeCh; ++c) sm.buf[lane][3 + c] = Gn[(size_t)k * kTreeCh + c];
           }
           __syncwarp();
-          if (on)
+          if (on) {
+            // software pipeline: distance + rsqrt of proxy j+1 overlap the contractions of proxy j
+            double gx = t.y0 - sm.buf[0][0], gy = t.y1 - sm.buf[0][1], gz = t.y2 - sm.buf[0][2];
+            double gri = rsqrt_nr(fma(gx, gx, fma(gy, gy, gz * gz)));
             for (int j = 0; j < nk; ++j) {
               const double* b = sm.buf[j];
-              const double dx = t.y0 - b[0], dy = t.y1 - b[1], dz = t.y2 - b[2];
-              const double ri = rsqrt_nr(fma(dx, dx, fma(dy, dy, dz * dz)));
+              const double* bn = sm.buf[j + 1 < nk ? j + 1 : j];
+              const double nx = t.y0 - bn[0], ny = t.y1 - bn[1], nz = t.y2 - bn[2];
+              const double nri = rsqrt_nr(fma(nx, nx, fma(ny, ny, nz * nz)));
+              const double dx = gx, dy = gy, dz = gz, ri = gri;
               const double ri2 = ri * ri;
               if (MODE & 1) {  // S (eq. 3) on g = G^fw - alpha G^nw
-                const double gx = fma(-t.alpha, b[6], b[3]), gy = fma(-t.alpha, b[7], b[4]),
-                             gz = fma(-t.alpha, b[8], b[5]);
-                const double a3 = fma(dx, gx, fma(dy, gy, dz * gz)) * ri2;
-                acc.u0 = fma(fma(dx, a3, gx), ri, acc.u0);
-                acc.u1 = fma(fma(dy, a3, gy), ri, acc.u1);
-                acc.u2 = fma(fma(dz, a3, gz), ri, acc.u2);
+                const double ux = fma(-t.alpha, b[6], b[3]), uy = fma(-t.alpha, b[7], b[4]),
+                             uz = fma(-t.alpha, b[8], b[5]);
+                const double a3 = fma(dx, ux, fma(dy, uy, dz * uz)) * ri2;
+                acc.u0 = fma(fma(dx, a3, ux), ri, acc.u0);
+                acc.u1 = fma(fma(dy, a3, uy), ri, acc.u1);
+                acc.u2 = fma(fma(dz, a3, uz), ri, acc.u2);
               }
               if (MODE & 2) {  // T (eq. 4) on D_ac = G^qn_ac - q0_a G^nw_c (the -6 in the finalize)
                 const double* Q = b + 9;
@@ -371,12 +381,14 @@ __global__ void __launch_bounds__(kTreeWarps * 32) tree_far_kernel(const TreeFar
                 acc.v1 = fma(dy, c, acc.v1);
                 acc.v2 = fma(dz, c, acc.v2);
               }
+              gx = nx; gy = ny; gz = nz; gri = nri;
             }
+          }
         }
       }
-      if (rmask) {
-        if (nd.nchild == 0) {  // leaf: direct far pairs for the rejecting lanes (near pairs: K3)
-          const bool on = rmask >> lane & 1;
+      if (dmask) {  // direct far pairs (near pairs masked: K3 owns them)
+        {
+          const bool on = dmask >> lane & 1;
           for (int j0 = nd.begin; j0 < nd.end; j0 += 32) {
             const int nj = min(32, nd.end - j0);
             __syncwarp();
@@ -393,7 +405,10 @@ __global__ void __launch_bounds__(kTreeWarps * 32) tree_far_kernel(const TreeFar
             const double rc2_lane = on ? p.rc2 : INFINITY;  // inactive lanes mask every pair
             for (int j = 0; j < nj; ++j) far_pair_masked<MODE>(load_src<MODE>(sm.buf[j]), t, acc, rc2_lane);
           }
-        } else {
+        }
+      }
+      if (rmask) {
+        {
           __syncwarp();
           if (lane == 0)
             for (int k = nd.nchild - 1; k >= 0; --k) {  // popped in octant order
