@@ -389,7 +389,7 @@ TreeWs tree_ws_layout(const Plan& P, int nnodes, int64_t N, int p) {
   return w;
 }
 
-template <int MODE>
+template <int MODE, bool SHARP>
 int run_eval_tree(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
                   const double* ty, const double* tb, const double* x0d, int64_t M, int64_t N, double h,
                   const double* rho, const stokes_er_tree_params* tp, const TreePlanHeader* hdr,
@@ -428,7 +428,7 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
     return STOKES_ER_ECUDA;
   pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, perm, src, srcbox);
   Delta3 r3{{rho[0], rho[1], rho[2]}};
-  pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, false, tgt, orig);
+  pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt, orig);
   {  // modified weights: leaves from their sources, then internal nodes level by level (M2M)
     const TreeNode* hn = reinterpret_cast<const TreeNode*>(plan + hdr->off_nodes);
     std::vector<int> sched;
@@ -457,7 +457,8 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   }
   if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
   const double dmax = rho[2] * h;
-  const double rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  const double cutoff = SHARP ? STOKES_ER_CUTOFF_SURFACE : STOKES_ER_CUTOFF;
+  const double rc2 = (cutoff * dmax) * (cutoff * dmax);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -473,13 +474,6 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   tfp.p = p;
   tfp.theta = tp->theta;
   tfp.rc2 = rc2;
-  {
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tree_far_kernel<MODE>, kTreeWarps * 32, 0);
-    const int grid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(tfp.n_groups, kTreeWarps), (int64_t)sms * std::max(occ, 1))));
-    tree_far_kernel<MODE><<<grid, kTreeWarps * 32, 0, s>>>(tfp);
-  }
   NearParams np;
   np.src = src;
   np.src_box = srcbox;
@@ -494,12 +488,13 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   np.rc2_box = rc2 * (1.0 + 1e-9);
   np.r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = 1.0 / (rho[k] * h);
-  {
+  {  // one persistent kernel: tree walks of the target groups + the near units
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_kernel<MODE, false>, kNearWarps * 32, 0);
-    const int ngrid = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(occ, 1))));
-    near_kernel<MODE, false><<<ngrid, kNearWarps * 32, 0, s>>>(np);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tree_far_kernel<MODE, SHARP>, kTreeWarps * 32, 0);
+    const int64_t work = (int64_t)tfp.n_groups + np.n_units;
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(work, kTreeWarps), (int64_t)sms * std::max(occ, 1))));
+    tree_far_kernel<MODE, SHARP><<<grid, kTreeWarps * 32, 0, s>>>(tfp, np, np.n_units);
   }
   finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad, 1, 32,
                                                           P.near_phases, out_u, out_v);
@@ -788,11 +783,11 @@ int stokes_er_eval_tree(const double* src_xyz, const double* src_normal, const d
   char* ws = static_cast<char*>(workspace);
   const char* pl = static_cast<const char*>(plan);
   switch (mode) {
-    case 1: return run_eval_tree<1>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
+    case 1: return run_eval_tree<1, false>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
                                     rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
-    case 2: return run_eval_tree<2>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
+    case 2: return run_eval_tree<2, false>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
                                     rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
-    default: return run_eval_tree<3>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N,
+    default: return run_eval_tree<3, false>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N,
                                      h, rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
   }
 }

@@ -30,6 +30,9 @@ constexpr int kTreeMaxDegree = 16;
 constexpr int kTreeCh = 15;               // fw(3) nw(3) q_a n_c w (9)
 constexpr int kTreeStack = 512;           // DFS stack entries per warp (depth <= 63)
 constexpr int kTreeWarps = 4;             // warps per CTA of tree_far_kernel
+#ifndef SER_TREE_MINB
+#define SER_TREE_MINB 4
+#endif
 constexpr uint64_t kTreeMagic = 0x53455254524545ULL;  // "SERTREE"
 
 struct TreeNode {  // POD, identical on host and device
@@ -277,20 +280,37 @@ struct __align__(16) TreeWarpSmem {
   double cosk[kTreeMaxDegree + 1];
 };
 
-// KT: far part of a warp's 32 targets (R23, R25); lane = target.
-template <int MODE>
-__global__ void __launch_bounds__(kTreeWarps * 32) tree_far_kernel(const TreeFarParams p) {
-  __shared__ TreeWarpSmem s_all[kTreeWarps];
+union TreeFusedSmem {
+  TreeWarpSmem t;
+  NearSmem n;
+};
+
+// KT: far part of a warp's 32 targets (R23, R25); lane = target.  The queue also
+// holds the n_near near units (K3 body), interleaved uniformly with the target
+// groups as in K13, so the latency-bound near pairs share the SMs with the
+// tree walk; the per-warp SMEM is a union of the two bodies.
+template <int MODE, bool SHARP>
+__global__ void __launch_bounds__(kTreeWarps * 32, SER_TREE_MINB) tree_far_kernel(const TreeFarParams p, const NearParams np,
+                                                                   int n_near) {
+  __shared__ TreeFusedSmem s_all[kTreeWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  TreeWarpSmem& sm = s_all[warp];
+  TreeWarpSmem& sm = s_all[warp].t;
   const int P1 = p.p + 1, NP = P1 * P1 * P1;
-  if (lane <= p.p) sm.cosk[lane] = cos(lane * kPi / p.p);
-  __syncwarp();
+  const int64_t total = (int64_t)p.n_groups + n_near;
   for (;;) {
-    int g = 0;
-    if (lane == 0) g = atomicAdd(p.counter, 1);
-    g = __shfl_sync(0xffffffffu, g, 0);
-    if (g >= p.n_groups) break;
+    int qi = 0;
+    if (lane == 0) qi = atomicAdd(p.counter, 1);
+    qi = __shfl_sync(0xffffffffu, qi, 0);
+    if (qi >= total) break;
+    int64_t idx;
+    if (fused_slot(qi, p.n_groups, n_near, &idx)) {
+      near_unit<MODE, SHARP>(np, static_cast<int>(idx), s_all[warp].n);
+      continue;
+    }
+    const int g = static_cast<int>(idx);
+    __syncwarp();
+    if (lane <= p.p) sm.cosk[lane] = cos(lane * kPi / p.p);
+    __syncwarp();
     const int64_t ti = (int64_t)g * 32 + lane;
     Tgt t;
     t.y0 = p.tgt[F_Y0 * p.Mpad + ti];
@@ -423,6 +443,7 @@ __global__ void __launch_bounds__(kTreeWarps * 32) tree_far_kernel(const TreeFar
     double* out = p.partial + (int64_t)g * 6 * 32 + lane;
     out[0] = acc.u0; out[32] = acc.u1; out[64] = acc.u2;
     out[96] = acc.v0; out[128] = acc.v1; out[160] = acc.v2;
+    __syncwarp();  // the warp's SMEM may hold a near unit next
   }
 }
 
