@@ -191,6 +191,13 @@ int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const dou
                       int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
                       void* stream, stokes_er_options* options);
 
+/* Treecode parameters (NEXT-3, Sec. 3.4; section below). */
+typedef struct {
+  int leaf_size;          /* N0: at most N0 points per leaf                          */
+  int degree;             /* p: Chebyshev degree per axis, 1..16                     */
+  double theta;           /* MAC parameter (0: never approximate = direct sum)       */
+} stokes_er_tree_params;
+
 /* ===================================================================== NEXT-2
  * Two-drop interfacial Stokes flow (Sec. 4.3): the
  * interface velocity u on two drops solves the integral equation (35)
@@ -246,9 +253,18 @@ typedef struct {
   double mu0;             /* exterior viscosity                                    */
   double tol;             /* GMRES relative residual                               */
   int max_iter;           /* Krylov dimension cap, 1..512                          */
+  int use_tree;           /* 0: direct sums; 1: every block through the treecode
+                             (NEXT-3, "We apply ... the treecode to all
+                             the integrals") with the plans below                 */
+  const void* tree_plan[2]; /* host plans (stokes_er_tree_build) over each drop's
+                             nodes, built with the same stokes_er_tree_params      */
+  const stokes_er_tree_params* tree; /* treecode parameters (use_tree = 1)        */
 } stokes_er_twodrop_params;
 
+/* Workspace for max_iter Krylov steps with direct sums (use_tree = 0). */
 size_t stokes_er_twodrop_workspace_bytes(int64_t N1, int64_t N2, int max_iter);
+/* Workspace for these parameters (either mode). */
+size_t stokes_er_twodrop_workspace_bytes_ex(int64_t N1, int64_t N2, const stokes_er_twodrop_params* params);
 int stokes_er_twodrop_setup(const stokes_er_drop drops[2], const stokes_er_cross cross[2],
                             const stokes_er_twodrop_params* params, void* workspace, size_t workspace_bytes,
                             void* stream);
@@ -286,11 +302,7 @@ int stokes_er_twodrop_solve(const stokes_er_drop drops[2], const stokes_er_cross
  * plan built for another N, degree > 16, or a tree over 8 N/N0 + 4096 nodes or
  * 63 levels.
  */
-typedef struct {
-  int leaf_size;          /* N0: at most N0 points per leaf                          */
-  int degree;             /* p: Chebyshev degree per axis, 1..16                     */
-  double theta;           /* MAC parameter (0: never approximate = direct sum)       */
-} stokes_er_tree_params;
+/* stokes_er_tree_params: see the NEXT-3 section below (declared here for NEXT-2). */
 
 size_t stokes_er_tree_plan_bytes(int64_t N, const stokes_er_tree_params* params);
 int stokes_er_tree_build(const double* src_xyz_host, int64_t N, const stokes_er_tree_params* params, void* plan,
@@ -303,6 +315,16 @@ int stokes_er_eval_tree(const double* src_xyz, const double* src_normal, const d
                         int64_t M, int64_t N, double h, const double rho[3], int mode,
                         const stokes_er_tree_params* params, const void* plan, double* out_u, double* out_v,
                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* NEXT-1 with the treecode: the on-surface s# evaluation of
+ * stokes_er_eval_onsurface (one delta, cutoff STOKES_ER_CUTOFF_SURFACE * delta)
+ * with the far part from the treecode (guard distance 7 delta).  Workspace:
+ * stokes_er_tree_workspace_bytes. */
+int stokes_er_eval_tree_onsurface(const double* src_xyz, const double* src_normal, const double* src_weight,
+                                  const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                                  const double* tgt_x0_density, int64_t M, int64_t N, double delta, int mode,
+                                  const stokes_er_tree_params* params, const void* plan, double* out_u,
+                                  double* out_v, void* workspace, size_t workspace_bytes, void* stream);
 
 const char* stokes_er_status_string(int status);
 int stokes_er_abi_version(void);

@@ -58,6 +58,8 @@ def lib():
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_eval_tree.argtypes = common + [_dp, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
                                                 ctypes.c_int, _dp, _dp, _dp]
+        L.oracle_eval_tree_sharp.argtypes = common + [ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                                                      ctypes.c_int, _dp, _dp, _dp]
         _lib = L
     return _lib
 
@@ -185,3 +187,16 @@ def evaluate_tree(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_
 
 def evaluate_tree_block(block, mode=BOTH, nthreads=0, **kw):
     return evaluate_tree(*block.arrays(), block.h, block.rho, mode=mode, nthreads=nthreads, **kw)
+
+
+def evaluate_tree_sharp(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, delta,
+                        leaf_size=2000, degree=6, theta=0.6, mode=BOTH, nthreads=0):
+    """NEXT-1's on-surface s# evaluation (single delta, cutoff 7) with the treecode far part."""
+    arrs, M, N = _inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density)
+    u = np.zeros((3, M)) if mode & SL else None
+    v = np.zeros((3, M)) if mode & DL else None
+    rc = lib().oracle_eval_tree_sharp(*[_p(a) for a in arrs], M, N, float(delta), int(mode), int(leaf_size),
+                                      int(degree), float(theta), int(nthreads), _p(u), _p(v), None)
+    if rc:
+        raise ValueError(f"oracle_eval_tree_sharp: status {rc}")
+    return u, v

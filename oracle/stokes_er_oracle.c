@@ -539,13 +539,18 @@ typedef struct {
  * degree p and MAC theta.  out_u, out_v: [3][M].  out_stats (may be NULL):
  * [0] nodes, [1] accepted (target, cluster) pairs, [2] directly summed
  * (target, source) pairs.  Returns 0, 1 (EINVAL) or 2 (tree too large). */
-int oracle_eval_tree(const double* src_xyz, const double* src_normal, const double* src_weight,
-                     const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
-                     const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
-                     int mode, int64_t N0, int p, double theta, int nthreads, double* out_u, double* out_v,
-                     double* out_stats) {
+/* sharp = 1: NEXT-1's on-surface single-delta s# evaluation (delta = h, rho
+ * ignored, cutoff 7 (R15), no extrapolation) with the same treecode far part. */
+static int eval_tree_impl(const double* src_xyz, const double* src_normal, const double* src_weight,
+                          const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                          const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho_in[3],
+                          int mode, int64_t N0, int p, double theta, int nthreads, int sharp, double* out_u,
+                          double* out_v, double* out_stats) {
+  const double one[3] = {1.0, 1.0, 1.0};
+  const double* rho = sharp ? one : rho_in;
   if (check_args(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, mode)) return 1;
-  if (!(rho[0] > 0.0 && rho[1] > rho[0] && rho[2] > rho[1]) || N0 < 1 || p < 1 || p > 40 || !(theta >= 0.0))
+  if ((!sharp && !(rho[0] > 0.0 && rho[1] > rho[0] && rho[2] > rho[1])) || N0 < 1 || p < 1 || p > 40 ||
+      !(theta >= 0.0))
     return 1;
   /* 1. tree (R22) */
   const int max_nodes = (int)(8 * (N / N0) + 4096);
@@ -606,7 +611,9 @@ int oracle_eval_tree(const double* src_xyz, const double* src_normal, const doub
   }
   /* 3. per target traversal */
   const double delta[3] = {rho[0] * h, rho[1] * h, rho[2] * h};
-  const double rc2 = (ORACLE_CUTOFF * delta[2]) * (ORACLE_CUTOFF * delta[2]);
+  const double cutoff = sharp ? 7.0 : ORACLE_CUTOFF;  /* R15 for s# */
+  const double rc2 = (cutoff * delta[2]) * (cutoff * delta[2]);
+  const int nd = sharp ? 1 : 3;
   double* ud = (double*)malloc(sizeof(double) * 9 * (size_t)(M > 0 ? M : 1));
   double* vd = (double*)malloc(sizeof(double) * 9 * (size_t)(M > 0 ? M : 1));
   double n_acc = 0.0, n_dir = 0.0;
@@ -678,23 +685,31 @@ int oracle_eval_tree(const double* src_xyz, const double* src_normal, const doub
         /* a leaf that fails, or an accepted cluster with no more points than
          * Chebyshev points (R26): direct sum, localized regularization */
         n_dir += (double)(t->end - t->begin);
-        accum_pairs(X, Nr, W, F, Q, N, t->begin, t->end, y, b, n0, x0, alpha, q0, delta, 3, mode, 1, 0, rc2,
+        accum_pairs(X, Nr, W, F, Q, N, t->begin, t->end, y, b, n0, x0, alpha, q0, delta, nd, mode, 1, sharp, rc2,
                     Us, Vs, Uf, Vf);
       } else {
         for (int k = t->nchild - 1; k >= 0; --k) stack[sp++] = t->first_child + k;  /* octant order */
       }
     }
     double U[3][3], V[3][3];
-    finish_target(b, q0, 3, Us, Vs, Uf, Vf, U, V);
-    for (int k = 0; k < 3; ++k)
+    finish_target(b, q0, nd, Us, Vs, Uf, Vf, U, V);
+    for (int k = 0; k < nd; ++k)
       for (int i = 0; i < 3; ++i) {
         ud[(k * 3 + i) * M + tg] = U[k][i];
         vd[(k * 3 + i) * M + tg] = V[k][i];
       }
   }
   int rc = 0;
-  if (M > 0 && (mode & 1)) rc = oracle_extrapolate(tgt_b, M, h, rho, ud, 3, out_u);
-  if (!rc && M > 0 && (mode & 2)) rc = oracle_extrapolate(tgt_b, M, h, rho, vd, 3, out_v);
+  if (sharp) { /* single delta: u^delta itself */
+    for (int64_t tg = 0; tg < M; ++tg)
+      for (int i = 0; i < 3; ++i) {
+        if (out_u && (mode & 1)) out_u[i * M + tg] = ud[i * M + tg];
+        if (out_v && (mode & 2)) out_v[i * M + tg] = vd[i * M + tg];
+      }
+  } else {
+    if (M > 0 && (mode & 1)) rc = oracle_extrapolate(tgt_b, M, h, rho, ud, 3, out_u);
+    if (!rc && M > 0 && (mode & 2)) rc = oracle_extrapolate(tgt_b, M, h, rho, vd, 3, out_v);
+  }
   if (out_stats) {
     out_stats[0] = T.nnodes;
     out_stats[1] = n_acc;
@@ -703,4 +718,21 @@ int oracle_eval_tree(const double* src_xyz, const double* src_normal, const doub
   free(ud); free(vd); free(X); free(Nr); free(W); free(F); free(Q);
   free(T.nodes); free(T.perm); free(T.mw);
   return rc;
+}
+
+int oracle_eval_tree(const double* src_xyz, const double* src_normal, const double* src_weight,
+                     const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                     const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
+                     int mode, int64_t N0, int p, double theta, int nthreads, double* out_u, double* out_v,
+                     double* out_stats) {
+  return eval_tree_impl(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode,
+                        N0, p, theta, nthreads, 0, out_u, out_v, out_stats);
+}
+
+int oracle_eval_tree_sharp(const double* src_xyz, const double* src_normal, const double* src_weight,
+                           const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                           const double* tgt_x0_density, int64_t M, int64_t N, double delta, int mode, int64_t N0,
+                           int p, double theta, int nthreads, double* out_u, double* out_v, double* out_stats) {
+  return eval_tree_impl(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, delta, NULL,
+                        mode, N0, p, theta, nthreads, 1, out_u, out_v, out_stats);
 }

@@ -28,7 +28,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import BOTH, DL, SL, evaluate, evaluate_sharp
+from . import BOTH, DL, SL, evaluate, evaluate_sharp, evaluate_tree, evaluate_tree_sharp
 
 INTERP_RADIUS = 3.5      # neighbours within 3.5 h of x0 (R20)
 INTERP_DEGREE = 4        # total degree in the tangent coordinates: 15 monomials
@@ -78,8 +78,11 @@ def interp_weights(nodes, x0, n0, h, radius=INTERP_RADIUS, degree=INTERP_DEGREE)
 class TwoDropOracle:
     """Operator, right-hand side and GMRES solve of IE (35) on the CPU."""
 
-    def __init__(self, td, localized=True, nthreads=0):
+    def __init__(self, td, localized=True, nthreads=0, tree=None):
+        """tree: None (direct localized sums) or (leaf_size, degree, theta): every block
+        through the treecode oracle (NEXT-3)."""
         self.td = td
+        self.tree = tree
         self.localized = localized
         self.nthreads = nthreads
         self.interp = []   # per drop b: interpolation stencils on drop 1-b at its nodes' x0
@@ -98,9 +101,12 @@ class TwoDropOracle:
         if q is not None:
             x0d[6:9] = q
         z = np.zeros((3, N))
-        return evaluate_sharp(d.x, d.n, d.w, f if f is not None else z, q if q is not None else z, d.x,
-                              np.zeros(N), x0d, self.td.delta_self, mode=mode, localized=self.localized,
-                              cutoff=CUTOFF_SHARP, nthreads=self.nthreads)
+        args = (d.x, d.n, d.w, f if f is not None else z, q if q is not None else z, d.x, np.zeros(N), x0d,
+                self.td.delta_self)
+        if self.tree is not None:
+            return evaluate_tree_sharp(*args, *self.tree, mode=mode, nthreads=self.nthreads)
+        return evaluate_sharp(*args, mode=mode, localized=self.localized, cutoff=CUTOFF_SHARP,
+                              nthreads=self.nthreads)
 
     def q0_cross(self, b, u_src):
         """u_{1-b} at the closest points x0 of drop b's nodes (R20)."""
@@ -119,9 +125,11 @@ class TwoDropOracle:
         if q is not None:
             x0d[6:9] = self.q0_cross(b, q)
         z = np.zeros((3, src.N))
-        return evaluate(src.x, src.n, src.w, f if f is not None else z, q if q is not None else z, tgt.x,
-                        cr.b, x0d, self.td.h, self.td.rho, mode=mode, localized=self.localized,
-                        nthreads=self.nthreads)
+        args = (src.x, src.n, src.w, f if f is not None else z, q if q is not None else z, tgt.x, cr.b, x0d,
+                self.td.h, self.td.rho)
+        if self.tree is not None:
+            return evaluate_tree(*args, *self.tree, mode=mode, nthreads=self.nthreads)
+        return evaluate(*args, mode=mode, localized=self.localized, nthreads=self.nthreads)
 
     # ---- IE (35) -----------------------------------------------------------------------
     def rhs(self):

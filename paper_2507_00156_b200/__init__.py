@@ -215,7 +215,10 @@ class TwoDropSolver:
     and float lam; cross: two dicts with b (N_b,) and x0d (6,N_b) (n0, [f](x0)) of
     drop b's nodes seen from drop 1-b (include/stokes_er.h)."""
 
-    def __init__(self, drops, cross, h, rho, delta_self, mu0=1.0, tol=1e-10, max_iter=100, stream=None):
+    def __init__(self, drops, cross, h, rho, delta_self, mu0=1.0, tol=1e-10, max_iter=100, stream=None,
+                 tree=None):
+        """tree: None (direct sums) or (leaf_size, degree, theta): every block through the
+        treecode (NEXT-3), with one TreePlan per drop."""
         torch = _torch()
         self.L = _lib.load()
         self._keep = (drops, cross)
@@ -233,7 +236,15 @@ class TwoDropSolver:
         self.cross = (_lib.Cross * 2)(*[_lib.Cross(_ptr(c["b"]), _ptr(c["x0d"])) for c in cross])
         self.params = _lib.TwoDropParams(float(h), (ctypes.c_double * 3)(*[float(r) for r in rho]),
                                          float(delta_self), float(mu0), float(tol), int(max_iter))
-        nbytes = int(self.L.stokes_er_twodrop_workspace_bytes(self.N[0], self.N[1], int(max_iter)))
+        self.plans = None
+        if tree is not None:
+            self.plans = [TreePlan(d["xyz"].cpu().numpy(), *tree) for d in drops]
+            self.tree_params = _lib.TreeParams(int(tree[0]), int(tree[1]), float(tree[2]))
+            self.params.use_tree = 1
+            self.params.tree_plan[0] = self.plans[0].buf.ctypes.data
+            self.params.tree_plan[1] = self.plans[1].buf.ctypes.data
+            self.params.tree = ctypes.pointer(self.tree_params)
+        nbytes = int(self.L.stokes_er_twodrop_workspace_bytes_ex(self.N[0], self.N[1], ctypes.byref(self.params)))
         if nbytes == 0:
             raise ValueError("stokes_er_twodrop_workspace_bytes: invalid sizes")
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -272,7 +283,7 @@ class TwoDropSolver:
         return out, int(iters.value), [float(hist[i]) for i in range(iters.value)]
 
 
-def twodrop_solver(td, device="cuda", max_iter=100, stream=None):
+def twodrop_solver(td, device="cuda", max_iter=100, stream=None, tree=None):
     """TwoDropSolver from a workloads.twodrop.TwoDrop input set (numpy arrays -> device)."""
     torch = _torch()
     dev = lambda a: torch.from_numpy(a).to(device)
@@ -281,7 +292,7 @@ def twodrop_solver(td, device="cuda", max_iter=100, stream=None):
     for c in td.cross:
         import numpy as np
         cross.append(dict(b=dev(c.b), x0d=dev(np.ascontiguousarray(np.concatenate([c.n0, c.f0], axis=0)))))
-    return TwoDropSolver(drops, cross, td.h, td.rho, td.delta_self, 1.0, td.tol, max_iter, stream)
+    return TwoDropSolver(drops, cross, td.h, td.rho, td.delta_self, 1.0, td.tol, max_iter, stream, tree)
 
 
 class TreePlan:
@@ -347,3 +358,29 @@ def evaluate_tree_block(block, plan=None, mode=BOTH, device="cuda", leaf_size=20
     if plan is None:
         plan = TreePlan(block.src_xyz, leaf_size, degree, theta)
     return evaluate_tree(*to_device(block, device), block.h, block.rho, plan, mode=mode, **kw)
+
+
+def evaluate_tree_onsurface(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, delta,
+                            plan: TreePlan, mode=BOTH, out_u=None, out_v=None, workspace=None, stream=None):
+    """stokes_er_eval_tree_onsurface: NEXT-1's s# evaluation with the treecode far part."""
+    torch = _torch()
+    M, N = _shapes(src_xyz, tgt_b)
+    dev = src_xyz.device
+    if plan.N != N:
+        raise ValueError("plan built for another node count")
+    L = _lib.load()
+    if mode & SL and out_u is None:
+        out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    if mode & DL and out_v is None:
+        out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+    if workspace is None:
+        nbytes = int(L.stokes_er_tree_workspace_bytes(M, N, mode, ctypes.byref(plan.params), plan.ptr()))
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    st = L.stokes_er_eval_tree_onsurface(_ptr(src_xyz), _ptr(src_normal), _ptr(src_weight),
+                                         _ptr(f if mode & SL else None), _ptr(q if mode & DL else None),
+                                         _ptr(tgt_xyz), _ptr(tgt_b), _ptr(tgt_x0_density), M, N, float(delta),
+                                         int(mode), ctypes.byref(plan.params), plan.ptr(),
+                                         _ptr(out_u if mode & SL else None), _ptr(out_v if mode & DL else None),
+                                         _ptr(workspace), int(workspace.numel()), _stream_handle(stream))
+    _lib.check("stokes_er_eval_tree_onsurface", st)
+    return (out_u if mode & SL else None), (out_v if mode & DL else None)

@@ -40,21 +40,22 @@ class Cross(ctypes.Structure):
     _fields_ = [("b", ctypes.c_void_p), ("x0d", ctypes.c_void_p)]
 
 
-class TwoDropParams(ctypes.Structure):
-    _fields_ = [("h", ctypes.c_double), ("rho", ctypes.c_double * 3), ("delta_self", ctypes.c_double),
-                ("mu0", ctypes.c_double), ("tol", ctypes.c_double), ("max_iter", ctypes.c_int)]
-
-
 class TreeParams(ctypes.Structure):
     _fields_ = [("leaf_size", ctypes.c_int), ("degree", ctypes.c_int), ("theta", ctypes.c_double)]
+
+
+class TwoDropParams(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_double), ("rho", ctypes.c_double * 3), ("delta_self", ctypes.c_double),
+                ("mu0", ctypes.c_double), ("tol", ctypes.c_double), ("max_iter", ctypes.c_int),
+                ("use_tree", ctypes.c_int), ("tree_plan", ctypes.c_void_p * 2), ("tree", ctypes.POINTER(TreeParams))]
 
 
 EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_er_eval", "stokes_er_eval_ex", "stokes_er_host_workspace_bytes",
            "stokes_er_eval_host", "stokes_er_eval_deltas", "stokes_er_eval_onsurface", "stokes_er_extrapolate", "stokes_er_launch_count",
            "stokes_er_status_string", "stokes_er_abi_version", "stokes_er_twodrop_workspace_bytes",
-           "stokes_er_twodrop_setup", "stokes_er_twodrop_rhs", "stokes_er_twodrop_apply", "stokes_er_twodrop_solve",
+           "stokes_er_twodrop_workspace_bytes_ex", "stokes_er_twodrop_setup", "stokes_er_twodrop_rhs", "stokes_er_twodrop_apply", "stokes_er_twodrop_solve",
            "stokes_er_tree_plan_bytes", "stokes_er_tree_build", "stokes_er_tree_info", "stokes_er_tree_workspace_bytes",
-           "stokes_er_eval_tree"]
+           "stokes_er_eval_tree", "stokes_er_eval_tree_onsurface"]
 
 _lib = None
 
@@ -98,6 +99,8 @@ def load():
     td = [ctypes.POINTER(Drop), ctypes.POINTER(Cross), ctypes.POINTER(TwoDropParams)]
     L.stokes_er_twodrop_workspace_bytes.argtypes = [_i64, _i64, ctypes.c_int]
     L.stokes_er_twodrop_workspace_bytes.restype = ctypes.c_size_t
+    L.stokes_er_twodrop_workspace_bytes_ex.argtypes = [_i64, _i64, ctypes.POINTER(TwoDropParams)]
+    L.stokes_er_twodrop_workspace_bytes_ex.restype = ctypes.c_size_t
     L.stokes_er_twodrop_setup.argtypes = td + [_dp, ctypes.c_size_t, _dp]
     L.stokes_er_twodrop_setup.restype = ctypes.c_int
     L.stokes_er_twodrop_rhs.argtypes = td + [_dp, _dp, ctypes.c_size_t, _dp]
@@ -119,6 +122,9 @@ def load():
     L.stokes_er_eval_tree.argtypes = [_dp] * 8 + [_i64, _i64, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
                                                   ctypes.c_int, tp, _dp, _dp, _dp, _dp, ctypes.c_size_t, _dp]
     L.stokes_er_eval_tree.restype = ctypes.c_int
+    L.stokes_er_eval_tree_onsurface.argtypes = [_dp] * 8 + [_i64, _i64, ctypes.c_double, ctypes.c_int, tp, _dp, _dp,
+                                                            _dp, _dp, ctypes.c_size_t, _dp]
+    L.stokes_er_eval_tree_onsurface.restype = ctypes.c_int
     _lib = L
     return L
 

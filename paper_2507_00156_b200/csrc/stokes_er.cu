@@ -763,12 +763,13 @@ size_t stokes_er_tree_workspace_bytes(int64_t M, int64_t N, int mode, const stok
   return tree_ws_layout(P, h->nnodes, N, params->degree).total;
 }
 
-int stokes_er_eval_tree(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
-                        const double* q, const double* tgt_xyz, const double* tgt_b, const double* tgt_x0_density,
-                        int64_t M, int64_t N, double h, const double rho[3], int mode,
-                        const stokes_er_tree_params* params, const void* plan, double* out_u, double* out_v,
-                        void* workspace, size_t workspace_bytes, void* stream) {
-  int st = validate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode);
+static int eval_tree_common(const double* src_xyz, const double* src_normal, const double* src_weight,
+                            const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                            const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
+                            int mode, const stokes_er_tree_params* params, const void* plan, double* out_u,
+                            double* out_v, void* workspace, size_t workspace_bytes, void* stream, bool sharp) {
+  int st = validate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode,
+                    !sharp);
   if (st) return st;
   if (!tree_params_ok(params)) return STOKES_ER_EINVAL;
   const TreePlanHeader* hdr = tree_header(plan, N);
@@ -782,14 +783,41 @@ int stokes_er_eval_tree(const double* src_xyz, const double* src_normal, const d
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(workspace);
   const char* pl = static_cast<const char*>(plan);
-  switch (mode) {
-    case 1: return run_eval_tree<1, false>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
-                                    rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
-    case 2: return run_eval_tree<2, false>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h,
-                                    rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
-    default: return run_eval_tree<3, false>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N,
-                                     h, rho, params, hdr, pl, out_u, out_v, ws, P, W, s);
+#define SER_TREE_RUN(M_, S_)                                                                                    \
+  run_eval_tree<M_, S_>(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, params, \
+                        hdr, pl, out_u, out_v, ws, P, W, s)
+  if (sharp) {
+    switch (mode) {
+      case 1: return SER_TREE_RUN(1, true);
+      case 2: return SER_TREE_RUN(2, true);
+      default: return SER_TREE_RUN(3, true);
+    }
   }
+  switch (mode) {
+    case 1: return SER_TREE_RUN(1, false);
+    case 2: return SER_TREE_RUN(2, false);
+    default: return SER_TREE_RUN(3, false);
+  }
+#undef SER_TREE_RUN
+}
+
+int stokes_er_eval_tree(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
+                        const double* q, const double* tgt_xyz, const double* tgt_b, const double* tgt_x0_density,
+                        int64_t M, int64_t N, double h, const double rho[3], int mode,
+                        const stokes_er_tree_params* params, const void* plan, double* out_u, double* out_v,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  return eval_tree_common(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, h, rho, mode,
+                          params, plan, out_u, out_v, workspace, workspace_bytes, stream, false);
+}
+
+int stokes_er_eval_tree_onsurface(const double* src_xyz, const double* src_normal, const double* src_weight,
+                                  const double* f, const double* q, const double* tgt_xyz, const double* tgt_b,
+                                  const double* tgt_x0_density, int64_t M, int64_t N, double delta, int mode,
+                                  const stokes_er_tree_params* params, const void* plan, double* out_u,
+                                  double* out_v, void* workspace, size_t workspace_bytes, void* stream) {
+  const double one[3] = {1.0, 1.0, 1.0};  // delta_1 = delta_2 = delta_3 = delta; weights (1, 0, 0)
+  return eval_tree_common(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, M, N, delta, one,
+                          mode, params, plan, out_u, out_v, workspace, workspace_bytes, stream, true);
 }
 
 }  // extern "C"

@@ -199,14 +199,18 @@ struct Layout {
   size_t off_V, off_w, off_partial, off_scalar, off_status, total;
 };
 
-Layout layout(int64_t N1, int64_t N2, int max_iter) {
+Layout layout(int64_t N1, int64_t N2, int max_iter, const stokes_er_twodrop_params* P = nullptr) {
   Layout L;
   L.N[0] = N1;
   L.N[1] = N2;
   L.n = 3 * (N1 + N2);
   L.max_iter = max_iter;
   for (int b = 0; b < 2; ++b)
-    for (int m = 0; m < 2; ++m) L.eval_ws = std::max(L.eval_ws, stokes_er_workspace_bytes(L.N[b], L.N[m], 3));
+    for (int m = 0; m < 2; ++m) {
+      L.eval_ws = std::max(L.eval_ws, stokes_er_workspace_bytes(L.N[b], L.N[m], 3));
+      if (P && P->use_tree)  // block (targets b <- sources m) through the treecode over drop m
+        L.eval_ws = std::max(L.eval_ws, stokes_er_tree_workspace_bytes(L.N[b], L.N[m], 3, P->tree, P->tree_plan[m]));
+    }
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -261,7 +265,13 @@ int validate(const stokes_er_drop* drops, const stokes_er_cross* cross, const st
     return STOKES_ER_EINVAL;
   if (!(P->rho[0] > 0.0 && P->rho[1] > P->rho[0] && P->rho[2] > P->rho[1] && std::isfinite(P->rho[2])))
     return STOKES_ER_EINVAL;
-  if (bytes < layout(drops[0].N, drops[1].N, P->max_iter).total) return STOKES_ER_EWORKSPACE;
+  if (P->use_tree) {
+    if (!P->tree) return STOKES_ER_EINVAL;
+    for (int m = 0; m < 2; ++m)
+      if (stokes_er_tree_workspace_bytes(drops[0].N, drops[m].N, 3, P->tree, P->tree_plan[m]) == 0)
+        return STOKES_ER_EINVAL;  // missing plan or one built for other nodes
+  }
+  if (bytes < layout(drops[0].N, drops[1].N, P->max_iter, P).total) return STOKES_ER_EWORKSPACE;
   return STOKES_ER_OK;
 }
 
@@ -292,13 +302,24 @@ int blocks(const Ctx& c, int mode, const double* u, double* out) {
                                                            Nb, x0c + 6 * Nb);
     }
     const bool sl = mode == STOKES_ER_SL;
-    st = stokes_er_eval_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr, sl ? nullptr : ub,
-                                  d[b].xyz, c.at<double>(c.L.off_zero[b]), x0s, Nb, Nb, c.P->delta_self, mode,
-                                  sl ? vs : nullptr, sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
+    if (c.P->use_tree)
+      st = stokes_er_eval_tree_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr,
+                                         sl ? nullptr : ub, d[b].xyz, c.at<double>(c.L.off_zero[b]), x0s, Nb, Nb,
+                                         c.P->delta_self, mode, c.P->tree, c.P->tree_plan[b], sl ? vs : nullptr,
+                                         sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
+    else
+      st = stokes_er_eval_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr, sl ? nullptr : ub,
+                                    d[b].xyz, c.at<double>(c.L.off_zero[b]), x0s, Nb, Nb, c.P->delta_self, mode,
+                                    sl ? vs : nullptr, sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
     if (st) break;
-    st = stokes_er_eval(d[m].xyz, d[m].normal, d[m].weight, sl ? d[m].f : nullptr, sl ? nullptr : um, d[b].xyz,
-                        c.cross[b].b, x0c, Nb, Nm, c.P->h, c.P->rho, mode, sl ? vc : nullptr, sl ? nullptr : vc,
-                        ews, c.L.eval_ws, c.s);
+    if (c.P->use_tree)
+      st = stokes_er_eval_tree(d[m].xyz, d[m].normal, d[m].weight, sl ? d[m].f : nullptr, sl ? nullptr : um,
+                               d[b].xyz, c.cross[b].b, x0c, Nb, Nm, c.P->h, c.P->rho, mode, c.P->tree,
+                               c.P->tree_plan[m], sl ? vc : nullptr, sl ? nullptr : vc, ews, c.L.eval_ws, c.s);
+    else
+      st = stokes_er_eval(d[m].xyz, d[m].normal, d[m].weight, sl ? d[m].f : nullptr, sl ? nullptr : um, d[b].xyz,
+                          c.cross[b].b, x0c, Nb, Nm, c.P->h, c.P->rho, mode, sl ? vc : nullptr, sl ? nullptr : vc,
+                          ews, c.L.eval_ws, c.s);
     if (st) break;
     const int64_t n3 = 3 * Nb;
     if (sl)  // rhs_b = -(2/mu0) (SL_bb + SL_bm)
@@ -344,12 +365,22 @@ size_t stokes_er_twodrop_workspace_bytes(int64_t N1, int64_t N2, int max_iter) {
   return layout(N1, N2, max_iter).total;
 }
 
+size_t stokes_er_twodrop_workspace_bytes_ex(int64_t N1, int64_t N2, const stokes_er_twodrop_params* params) {
+  if (!params || N1 < 1 || N2 < 1 || params->max_iter < 1 || params->max_iter > 512) return 0;
+  if (params->use_tree) {
+    if (!params->tree) return 0;
+    for (int m = 0; m < 2; ++m)
+      if (stokes_er_tree_workspace_bytes(N1, m ? N2 : N1, 3, params->tree, params->tree_plan[m]) == 0) return 0;
+  }
+  return layout(N1, N2, params->max_iter, params).total;
+}
+
 int stokes_er_twodrop_setup(const stokes_er_drop drops[2], const stokes_er_cross cross[2],
                             const stokes_er_twodrop_params* params, void* workspace, size_t workspace_bytes,
                             void* stream) {
   int st = validate(drops, cross, params, workspace, workspace_bytes);
   if (st || (st = arch_ok())) return st;
-  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter), static_cast<char*>(workspace),
+  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter, params), static_cast<char*>(workspace),
         static_cast<cudaStream_t>(stream)};
   int* status = c.at<int>(c.L.off_status);
   if ((st = ok(cudaMemsetAsync(status, 0, 4 * sizeof(int), c.s)))) return st;
@@ -387,7 +418,7 @@ int stokes_er_twodrop_rhs(const stokes_er_drop drops[2], const stokes_er_cross c
   int st = validate(drops, cross, params, workspace, workspace_bytes);
   if (st || (st = arch_ok())) return st;
   if (!out_rhs) return STOKES_ER_EINVAL;
-  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter), static_cast<char*>(workspace),
+  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter, params), static_cast<char*>(workspace),
         static_cast<cudaStream_t>(stream)};
   return blocks(c, STOKES_ER_SL, nullptr, out_rhs);
 }
@@ -398,7 +429,7 @@ int stokes_er_twodrop_apply(const stokes_er_drop drops[2], const stokes_er_cross
   int st = validate(drops, cross, params, workspace, workspace_bytes);
   if (st || (st = arch_ok())) return st;
   if (!u || !out_Au || u == out_Au) return STOKES_ER_EINVAL;
-  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter), static_cast<char*>(workspace),
+  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter, params), static_cast<char*>(workspace),
         static_cast<cudaStream_t>(stream)};
   return blocks(c, STOKES_ER_DL, u, out_Au);
 }
@@ -409,7 +440,7 @@ int stokes_er_twodrop_solve(const stokes_er_drop drops[2], const stokes_er_cross
   int st = validate(drops, cross, params, workspace, workspace_bytes);
   if (st || (st = arch_ok())) return st;
   if (!out_u) return STOKES_ER_EINVAL;
-  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter), static_cast<char*>(workspace),
+  Ctx c{drops, cross, params, layout(drops[0].N, drops[1].N, params->max_iter, params), static_cast<char*>(workspace),
         static_cast<cudaStream_t>(stream)};
   const int K = params->max_iter;
   const int64_t n = c.L.n;

@@ -93,3 +93,21 @@ def test_tree_plan_reuse_and_errors(ser):
     other = ser.TreePlan(blk.src_xyz[:, :100], 300, 6, 0.6)
     with pytest.raises(ValueError):
         ser.evaluate_tree(*arrs, blk.h, blk.rho, other)
+
+
+def test_tree_onsurface_parity(ser):
+    """NEXT-1 s# with the treecode far part (config 5 at 1/h = 64, delta = 3h, cutoff 7):
+    against oracle_eval_tree_sharp on sampled targets, and theta = 0 against the direct s# path."""
+    blk = config5(inv_h=64)
+    d = 3 * blk.h
+    plan = ser.TreePlan(blk.src_xyz, 2000, 6, 0.6)
+    arrs = ser.to_device(blk)
+    u, v = ser.evaluate_tree_onsurface(*arrs, d, plan)
+    idx = np.arange(0, blk.M, 263)
+    sub = blk.take_targets(idx)
+    ur, vr = oracle.evaluate_tree_sharp(*sub.arrays(), d, leaf_size=2000, degree=6, theta=0.6)
+    assert rel(u.cpu().numpy()[:, idx], ur) <= TOL and rel(v.cpu().numpy()[:, idx], vr) <= TOL
+    plan0 = ser.TreePlan(blk.src_xyz, 2000, 6, 0.0)
+    u0, v0 = ser.evaluate_tree_onsurface(*arrs, d, plan0)
+    ud, vd = ser.evaluate_onsurface(*arrs, d)
+    assert rel(u0.cpu().numpy(), ud.cpu().numpy()) <= 1e-13 and rel(v0.cpu().numpy(), vd.cpu().numpy()) <= 1e-13

@@ -127,3 +127,23 @@ def test_self_convergence_matches_oracle_golden(ser):
     mag = np.linalg.norm(e, axis=0)
     assert abs(mag.max() / g["max_err"]["8"] - 1.0) <= 1e-6
     assert abs(np.sqrt((mag ** 2).mean()) / g["l2_err"]["8"] - 1.0) <= 1e-6
+
+
+def test_twodrop_with_treecode_parity(ser):
+    """NEXT-2 + NEXT-3 (the treecode on all the integrals): every block
+    through the treecode on both sides (N0 300, p 8, theta 0.6) at 1/h = 16: rhs and
+    A u to 1e-12, the solve to 1e-8 with the same iteration count."""
+    import torch
+
+    from oracle.twodrop import TwoDropOracle
+
+    td = twodrop(16)
+    tree = (300, 8, 0.6)
+    o = TwoDropOracle(td, tree=tree)
+    s = ser.twodrop_solver(td, tree=tree)
+    assert rel(s.rhs().cpu().numpy(), o.rhs()) <= 1e-12
+    u = np.random.default_rng(3).uniform(-1, 1, td.n_unknowns)
+    assert rel(s.apply(torch.from_numpy(u).cuda()).cpu().numpy(), o.apply(u)) <= 1e-12
+    ug, it, _ = s.solve()
+    uo, ito, _ = o.solve()
+    assert it == ito and rel(ug.cpu().numpy(), uo) <= 1e-8

@@ -21,13 +21,28 @@ import torch  # noqa: E402
 import paper_2507_00156_b200 as ser  # noqa: E402
 from workloads.twodrop import match_nodes, split, twodrop  # noqa: E402
 
-out_path = sys.argv[1] if len(sys.argv) > 1 else None
-levels = [int(a) for a in sys.argv[2:]] or [16, 32, 64, 128]
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+use_tree = "--tree" in sys.argv  # every block through the treecode with the eq. (33) policy
+out_path = args[0] if args else None
+levels = [int(a) for a in args[1:]] or [16, 32, 64, 128]
+
+
+TABLE2 = {16: (1000, 6), 32: (1000, 6), 64: (2000, 8), 128: (4000, 10), 256: (8000, 12)}
+
+
+def policy(inv_h):
+    """Treecode parameters of PAPER.md Table 2 (theta 0.6, N0 and p per row, lines 359-363);
+    other h: eq. (33) (h = 1/64: N0 2000, p 6; h -> h/2: N0 x 2, p + 2)."""
+    if inv_h in TABLE2:
+        return (*TABLE2[inv_h], 0.6)
+    k = int(round(np.log2(inv_h / 64)))
+    return (int(2000 * 2.0 ** k), max(2, 6 + 2 * k), 0.6)
+
 rows, sol = [], {}
 for ih in levels:
     td = twodrop(ih)
     t0 = time.perf_counter()
-    s = ser.twodrop_solver(td)
+    s = ser.twodrop_solver(td, tree=policy(ih) if use_tree else None)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     s.solve()  # warm-up (also checks convergence)
@@ -40,7 +55,7 @@ for ih in levels:
     N = [d.N for d in td.drops]
     pairs_matvec = sum(N[i] * N[j] for i in range(2) for j in range(2))  # 4 blocks
     sol[ih] = (td, u.cpu().numpy())
-    rows.append({"inv_h": ih, "N_per_drop": N, "iterations": it, "final_residual": hist[-1],
+    rows.append({"inv_h": ih, "N_per_drop": N, "tree": policy(ih) if use_tree else None, "iterations": it, "final_residual": hist[-1],
                  "solve_ms": ms, "setup_s": t_setup, "block_evals": 4 * (it + 1),
                  "pairs_per_solve": pairs_matvec * (it + 1),
                  "pairs_per_s": pairs_matvec * (it + 1) / (ms / 1e3), "u_max": float(np.abs(u.cpu().numpy()).max())})
@@ -67,7 +82,8 @@ for r, r2 in zip(rows, rows[1:]):
         for rad in (0.1, 0.25, 0.5):
             k = f"max_err_away_{rad}"
             r2[f"order_away_{rad}"] = float(np.log2(r[k] / r2[k]))
-res = {"what": "PAPER.md Table 2 on one B200: two-drop IE (35), GMRES tol 1e-10, direct (no treecode) sums",
+res = {"what": "PAPER.md Table 2 on one B200: two-drop IE (35), GMRES tol 1e-10, "
+               + ("treecode (Table 2 parameters) on every block" if use_tree else "direct (no treecode) sums"),
        "paper_table2": {"16": [13, 3.17e-3, 1.19e-4], "32": [12, 1.07e-4, 6.11e-6], "64": [12, 4.06e-6, 2.11e-7],
                         "128": [12, 1.02e-7, 6.37e-9], "columns": ["iterations", "max err", "L2 err"]},
        "gpu": torch.cuda.get_device_name(), "rows": rows}
