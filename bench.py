@@ -200,6 +200,22 @@ def cpu_baseline(block):
                       f"(paper's shared-far-field algorithm), {dt:.1f} s wall"}
 
 
+def committed_traffic(fused: bool):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
+    `ncu --set full` summary of this bench command (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_v10_fused.json")
+    if not fused or not os.path.exists(path):
+        return None
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for k in json.load(open(path))["kernels"]:
+        if k["kernel"].startswith("void fused_kernel<3, 2"):
+            tot = 0.0
+            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v, u = k[key].split()
+                tot += float(v) * units[u]
+            return int(tot), "profiles/r01/ncu_full_v10_fused.json (one ncu --set full capture of this command)"
+    return None
+
 def twodrop_launches(it: int) -> int:
     """Our kernel launches in one stokes_er_twodrop_solve that took `it` Krylov steps."""
     per_eval = 7
@@ -480,6 +496,9 @@ def main():
                 "kernel_ms": far_avg_s * 1e3,
                 "kernel_share": sum(pair_ms) / sum(step_ms),
                 "far_pairs": far, "near_pairs": near}
+    traffic = committed_traffic(fused)
+    if traffic:
+        roofline["traffic"], roofline["traffic_source"] = traffic
     if clocks.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (SMS * FP64_LANES_PER_SM * 2 * clocks["sm_mhz"] / 1e6)
     if fused:
