@@ -135,6 +135,23 @@ def test_config5_h128_sampled(ser):
     assert eu <= TOL and ev <= TOL
 
 
+def test_config5_h256_max_size_sampled(ser):
+    """The largest configuration (BASELINE.json config 5 at 1/h = 256: N = M = 1,090,854),
+    full GPU evaluation, 48 sampled targets against the definition-mode oracle."""
+    eu, ev = _sampled(ser, config5(inv_h=256), k=48)
+    assert eu <= TOL and ev <= TOL
+
+
+def test_config3_h128_and_config4_h64_sampled(ser):
+    """BASELINE.json configs 3 and 4 at their full sizes (ellipsoid 1/h = 128; two spheres
+    at 1/h = 64, eps = 0.05, all four blocks)."""
+    eu, ev = _sampled(ser, config3(inv_h=128), k=96)
+    assert eu <= TOL and ev <= TOL
+    for blk in config4(eps=0.05, inv_h=64):
+        eu, ev = _sampled(ser, blk, k=64)
+        assert eu <= TOL and ev <= TOL, blk.name
+
+
 def test_tunings_agree(ser):
     """targets/thread 2 vs 4 and different source chunkings: same sums up to rounding order."""
     blk = config2(inv_h=32)
