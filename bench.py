@@ -67,8 +67,10 @@ def parse():
 
 
 def make_workload(cfg: int, inv_h: int, rank: int):
-    from workloads.configs import config1, config2, config3, config5
+    from workloads.configs import config1, config2, config3, config5, pure_far
     seed = cfg + 1000 * rank
+    if cfg == 6:  # pure-far micro-config isolating the far-field pair sum
+        return pure_far(inv_h=inv_h, seed=seed)
     if cfg == 1:
         return config1(seed=seed)
     if cfg == 2:
@@ -77,7 +79,7 @@ def make_workload(cfg: int, inv_h: int, rank: int):
         return config3(inv_h=inv_h, seed=seed)
     if cfg == 5:
         return config5(inv_h=inv_h, seed=seed)
-    raise SystemExit("bench configs: 1, 2, 3, 5 (config 4 is a 4-block parity case)")
+    raise SystemExit("bench configs: 1, 2, 3, 5, 6 = pure far (config 4 is a 4-block parity case)")
 
 
 def near_pair_count(block) -> int:
