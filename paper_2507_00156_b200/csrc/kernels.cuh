@@ -49,6 +49,7 @@ constexpr int kSub = 32;             // sources per classification sub-tile
 constexpr int kSrcDoubles = 12;      // packed source record: x(3) mw(3) fw(3) q(3)
 constexpr int kTgtFields = 14;       // y(3) alpha q0(3) n0(3) b w(3)
 constexpr int kTileBytes = kTile * kSrcDoubles * 8;
+constexpr int kFarSmemBytes = 2 * kTileBytes;  // far-item TMA double buffer
 constexpr double kPartialCapBytes = 256.0 * 1024 * 1024;
 
 enum TgtField { F_Y0 = 0, F_Y1, F_Y2, F_ALPHA, F_Q0, F_Q1, F_Q2, F_N0, F_N1, F_N2, F_B, F_W0, F_W1, F_W2 };
@@ -528,7 +529,8 @@ template <int MODE, int T>
 #define SER_FAR_MINB (512 / SER_FAR_THREADS)
 #endif
 __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) far_kernel(const PairParams p) {
-  __shared__ __align__(128) double tile[2][kTile * kSrcDoubles];
+  extern __shared__ __align__(128) unsigned char far_smem[];  // kFarSmemBytes (dynamic)
+  auto* tile = reinterpret_cast<double(*)[kTile * kSrcDoubles]>(far_smem);
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int s_item;
   if (threadIdx.x == 0) {
@@ -814,7 +816,6 @@ __global__ void __launch_bounds__(kNearWarps * 32, SER_NEAR_MINB) near_kernel(co
 // latency-bound near pairs and the far warps fill the near warps' stalls; the
 // rest follow the last far item and fill the tail.  The
 // SMEM of the two bodies is a union; the item counter is PairParams::counter.
-constexpr int kFarSmemBytes = 2 * kTile * kSrcDoubles * 8;
 constexpr int kNearSmemBytes = kNearWarps * (int)sizeof(NearSmem);
 constexpr int kFusedSmemBytes = kFarSmemBytes > kNearSmemBytes ? kFarSmemBytes : kNearSmemBytes;
 #ifndef SER_NEAR_TAIL_PCT
@@ -837,7 +838,7 @@ template <int MODE, int T, bool SHARP>
 __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) fused_kernel(const PairParams p, const NearParams np,
                                                                        int n_near_items) {
   static_assert(kThreads == kNearWarps * 32, "fused kernel: one near unit per warp");
-  __shared__ __align__(128) unsigned char smem[kFusedSmemBytes];
+  extern __shared__ __align__(128) unsigned char smem[];  // kFusedSmemBytes (dynamic: may exceed 48 KB)
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ int s_item;
   auto* tile = reinterpret_cast<double(*)[kTile * kSrcDoubles]>(smem);

@@ -231,19 +231,21 @@ void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, far_kernel<MODE, T>, kThreads, 0);
+  cudaFuncSetAttribute(far_kernel<MODE, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFarSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, far_kernel<MODE, T>, kThreads, kFarSmemBytes);
   const int grid = std::max(1, std::min(pp.n_items, sms * std::max(occ, 1)));
   *grid_out = grid;
-  far_kernel<MODE, T><<<grid, kThreads, 0, s>>>(pp);
+  far_kernel<MODE, T><<<grid, kThreads, kFarSmemBytes, s>>>(pp);
 }
 
 template <int MODE, int T, bool SHARP>
 int launch_fused(const PairParams& pp, const NearParams& np, int n_near_items, int sms, cudaStream_t s) {
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<MODE, T, SHARP>, kThreads, 0);
+  cudaFuncSetAttribute(fused_kernel<MODE, T, SHARP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<MODE, T, SHARP>, kThreads, kFusedSmemBytes);
   const int64_t work = (int64_t)pp.n_items + n_near_items;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)sms * std::max(occ, 1))));
-  fused_kernel<MODE, T, SHARP><<<grid, kThreads, 0, s>>>(pp, np, n_near_items);
+  fused_kernel<MODE, T, SHARP><<<grid, kThreads, kFusedSmemBytes, s>>>(pp, np, n_near_items);
   return grid;
 }
 
