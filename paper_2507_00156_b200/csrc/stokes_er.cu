@@ -715,6 +715,8 @@ int stokes_er_tree_build(const double* src_xyz_host, int64_t N, const stokes_er_
                          size_t plan_bytes) {
   if (!src_xyz_host || N < 1 || N > INT32_MAX || !tree_params_ok(params) || !plan) return STOKES_ER_EINVAL;
   if (plan_bytes < tree_plan_bytes(N, params->leaf_size)) return STOKES_ER_EWORKSPACE;
+  for (int64_t j = 0; j < 3 * N; ++j)
+    if (!std::isfinite(src_xyz_host[j])) return STOKES_ER_EINVAL;  // the midpoint splits need finite nodes
   TreeBuilder b;
   b.x = src_xyz_host;
   b.N = N;
