@@ -295,3 +295,46 @@ def test_delta_power_schedule_parity(ser):
     h_eff = blk.h ** 0.8 * (1.0 / 16) ** 0.2
     b2 = dataclasses.replace(blk, h=h_eff)
     check_block(ser, b2.take_targets(np.arange(0, b2.M, 7)), localized=True)
+
+
+def test_mode_composition_and_linearity(ser):
+    """Properties: the SL-only and DL-only calls give the BOTH call's u and
+    v; the map (f, q) -> (u, v) is linear (the subtraction terms use f(x0), q(x0) of
+    the same fields)."""
+    import dataclasses
+
+    blk = config2(inv_h=32)
+    u3, v3 = run_gpu(ser, blk, mode=3)
+    u1, _ = run_gpu(ser, blk, mode=1)
+    _, v2 = run_gpu(ser, blk, mode=2)
+    assert rel(u1, u3) <= 1e-14 and rel(v2, v3) <= 1e-14
+    from workloads.densities import PolyField
+
+    rng = np.random.default_rng(77)  # same geometry, other seeded cubic densities
+    F, Q = PolyField(rng), PolyField(rng)
+    x0d = np.concatenate([blk.tgt_x0_density[:3], F(blk.tgt_x0), Q(blk.tgt_x0)])
+    other = dataclasses.replace(blk, f=np.ascontiguousarray(F(blk.src_xyz)), q=np.ascontiguousarray(Q(blk.src_xyz)),
+                                tgt_x0_density=np.ascontiguousarray(x0d))
+    a, b = 0.7, -1.3
+    mix = dataclasses.replace(blk, f=a * blk.f + b * other.f, q=a * blk.q + b * other.q,
+                              tgt_x0_density=np.ascontiguousarray(np.concatenate(
+                                  [blk.tgt_x0_density[:3], a * blk.tgt_x0_density[3:] + b * other.tgt_x0_density[3:]])))
+    um, vm = run_gpu(ser, mix)
+    uo, vo = run_gpu(ser, other)
+    assert rel(um, a * u3 + b * uo) <= 1e-13 and rel(vm, a * v3 + b * vo) <= 1e-13
+
+
+def test_target_shards_concatenate(ser):
+    """Multi-GPU sharding simulated on one GPU: the contiguous target ranges
+    of paper_2507_00156_b200.sharding evaluated separately concatenate to the full run."""
+    from paper_2507_00156_b200.sharding import shard_bounds
+
+    blk = config2(inv_h=32)
+    u, v = run_gpu(ser, blk)
+    parts = []
+    for r in range(3):
+        a, b = shard_bounds(blk.M, r, 3)
+        parts.append(run_gpu(ser, blk.take_targets(np.arange(a, b))))
+    us = np.concatenate([p[0] for p in parts], axis=1)
+    vs = np.concatenate([p[1] for p in parts], axis=1)
+    assert rel(us, u) <= 1e-13 and rel(vs, v) <= 1e-13
