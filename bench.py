@@ -57,9 +57,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
     ap.add_argument("--near-phases", type=int, default=0)
-    ap.add_argument("--workload", choices=["eval", "twodrop"], default="eval",
+    ap.add_argument("--workload", choices=["eval", "twodrop", "tree"], default="eval",
                     help="eval: one stokes_er_eval of BASELINE.json config --config (default); "
-                         "twodrop: one GMRES solve of the NEXT-2 two-drop IE (35) at 1/h = --inv-h")
+                         "twodrop: one GMRES solve of the NEXT-2 two-drop IE (35) at 1/h = --inv-h; "
+                         "tree: one stokes_er_eval_tree (NEXT-3) of config --config at 1/h = --inv-h")
+    ap.add_argument("--tree", type=str, default="",
+                    help="treecode N0,p,theta (default: PAPER.md eq. (33) policy for --inv-h)")
     ap.add_argument("--schedule", choices=["fused", "separate"], default="fused",
                     help="fused: one persistent kernel, far items and near items from one interleaved "
                          "queue (default); separate: far kernel then near kernel")
@@ -227,6 +230,97 @@ def twodrop_launches(it: int) -> int:
         n += 3 * (j + 1) + 3                # MGS: dot (2) + update (1) per basis vector; norm + scale
     return n + it                           # u = V y
 
+F_PROXY_ALG = 77  # algorithmic flops of one target-proxy interaction of eq. (31): a far pair's 57 with the
+                  # DL contraction over the 9 q_a n_c w channels (41 flops) in place of the 3-vector form (21)
+
+
+def run_tree(args, rank, world):
+    """NEXT-3 bench: one step = one stokes_er_eval_tree (plan reused: the octree depends on the
+    nodes only) of config --config at 1/h = --inv-h; value = direct-equivalent pair
+    interactions per second (M N / time); accuracy against the direct path in the same run."""
+    import ctypes
+
+    import torch
+
+    import paper_2507_00156_b200 as ser
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    block = make_workload(args.config, args.inv_h, rank)
+    M, N = block.M, block.N
+    if args.tree:
+        n0, p, th = args.tree.split(",")
+        tp = (int(n0), int(p), float(th))
+    else:  # PAPER.md eq. (33): theta 0.6, N0 2000 and p 6 at h = 1/64, N0 x 2 and p + 2 per halving
+        k = int(round(math.log2(args.inv_h / 64)))
+        tp = (int(2000 * 2.0 ** k), max(2, 6 + 2 * k), 0.6)
+    t0 = time.perf_counter()
+    plan = ser.TreePlan(block.src_xyz, *tp)
+    t_plan = time.perf_counter() - t0
+    arrs = ser.to_device(block, dev)
+    u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    v = torch.empty((3, M), dtype=torch.float64, device=dev)
+    nbytes = int(ser._lib.load().stokes_er_tree_workspace_bytes(M, N, 3, ctypes.byref(plan.params), plan.ptr()))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        flush.zero_()
+        ser.evaluate_tree(*arrs, block.h, block.rho, plan, out_u=u, out_v=v, workspace=ws)
+    torch.cuda.synchronize(dev)
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(K):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ser.evaluate_tree(*arrs, block.h, block.rho, plan, out_u=u, out_v=v, workspace=ws)
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    from paper_2507_00156_b200.sharding import max_over_ranks
+    total_s = max_over_ranks(sum(ms) / 1e3, dev)
+    ud, vd = ser.evaluate(*arrs, block.h, block.rho)
+    torch.cuda.synchronize(dev)
+    diff = max(float((u - ud).abs().max() / ud.abs().max()), float((v - vd).abs().max() / vd.abs().max()))
+    if rank != 0:
+        return None
+    # work counts from the treecode oracle on a target sample (per-target traversal statistics)
+    import oracle
+    rng = np.random.default_rng(0)
+    idx = rng.choice(M, min(M, 128), replace=False)
+    _, _, st = oracle.evaluate_tree_block(block.take_targets(idx), leaf_size=tp[0], degree=tp[1], theta=tp[2],
+                                          stats=True)
+    proxies = st[1] / len(idx) * (tp[1] + 1) ** 3 * M
+    direct = st[2] / len(idx) * M
+    near = near_pair_count(block)
+    flops = proxies * F_PROXY_ALG + (direct - near) * F_FAR_ALG + near * F_NEAR_ALG
+    peak = SMS * FP64_LANES_PER_SM * 2 * 1965.0 * 1e6 / 1e12
+    achieved = flops / (total_s / K) / 1e12
+    line = {"metric": "treecode (NEXT-3) SL+DL 3-delta evaluation: direct-equivalent pair interactions/sec (M N / time)",
+            "value": world * M * N * K / total_s, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": block.name + "_treecode", "N": N, "M": M, "N0": tp[0], "p": tp[1],
+                       "theta": tp[2], "tree_nodes": plan.nodes, "tree_depth": plan.depth,
+                       "host_plan_build_s": t_plan, "max_rel_diff_vs_direct": diff,
+                       "proxy_interactions_per_step": proxies, "direct_pairs_per_step": direct,
+                       "near_pairs_per_step": near, "work_counts": "oracle traversal statistics on 128 targets",
+                       "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "whole treecode evaluation (P2M/M2M, tree walk + near units, finalize): "
+                                   f"{F_PROXY_ALG} flops per target-proxy interaction, {F_FAR_ALG} per direct far "
+                                   f"pair, {F_NEAR_ALG} per near pair",
+                         "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz"},
+            "clocks": clk.summary(), "gpu_launches": K * 9,
+            "gpu_launches_note": "per step: bbox, morton, pack sources, pack targets, P2M, M2M per level (<= 3), "
+                                 "tree walk + near units, finalize (+ CUB sort)",
+            "e2e": None}
+    return line
+
+
 def run_twodrop(args, rank, world):
     """NEXT-2 bench: one step = one full GMRES solve of IE (35) (Sec. 4.3)
     on the two drops at 1/h = args.inv_h through stokes_er_twodrop_solve: 4 block
@@ -356,6 +450,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.workload == "tree" and args.impl == "ours":
+        line = run_tree(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
 
     if args.workload == "twodrop" and args.impl == "ours":
         line = run_twodrop(args, rank, world)
