@@ -12,5 +12,5 @@ for _ in range(2):
 torch.cuda.synchronize()
 PY
 timeout 300 python /tmp/tree_one.py 128 4000 8 && echo clean-ok
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tree_far|near_kernel" -c 2 -o gpurun_out/tree_full python /tmp/tree_one.py 128 4000 8 > gpurun_out/tree_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tree_far" -c 1 -o gpurun_out/tree_full python /tmp/tree_one.py 128 4000 8 > gpurun_out/tree_ncu.log 2>&1
 echo "ncu rc=$?"
