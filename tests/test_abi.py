@@ -63,3 +63,29 @@ def test_product_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, fn)).read()
                 assert "import oracle" not in text and "from oracle" not in text and "liboracle" not in text, fn
+
+
+def _build_c_demo(tmp_path):
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "c_api_demo")
+    pkg = os.path.join(root, "paper_2507_00156_b200")
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                           os.path.join(root, "examples", "c_api_demo.c"), "-L", pkg, "-lstokes_er",
+                           "-L", "/usr/local/cuda/lib64", "-lcudart", "-lm", f"-Wl,-rpath,{pkg}", "-o", exe])
+    return exe
+
+
+def test_c_demo_compiles_against_the_header(tmp_path):
+    """The boundary is usable from plain C: examples/c_api_demo.c compiles and links
+    against include/stokes_er.h and libstokes_er.so (no torch, no Python)."""
+    assert os.path.exists(_build_c_demo(tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_demo_runs(tmp_path):
+    import subprocess
+
+    out = subprocess.run([_build_c_demo(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
