@@ -57,10 +57,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
     ap.add_argument("--near-phases", type=int, default=0)
-    ap.add_argument("--workload", choices=["eval", "twodrop", "tree"], default="eval",
+    ap.add_argument("--workload", choices=["eval", "twodrop", "tree", "spheroid"], default="eval",
                     help="eval: one stokes_er_eval of BASELINE.json config --config (default); "
                          "twodrop: one GMRES solve of the NEXT-2 two-drop IE (35) at 1/h = --inv-h; "
-                         "tree: one stokes_er_eval_tree (NEXT-3) of config --config at 1/h = --inv-h")
+                         "tree: one stokes_er_eval_tree (NEXT-3) of config --config at 1/h = --inv-h; "
+                         "spheroid: PAPER.md Table 1's SL evaluation at 1/h = --inv-h")
     ap.add_argument("--tree", type=str, default="",
                     help="treecode N0,p,theta (default: PAPER.md eq. (33) policy for --inv-h)")
     ap.add_argument("--schedule", choices=["fused", "separate"], default="fused",
@@ -321,6 +322,67 @@ def run_tree(args, rank, world):
     return line
 
 
+# PAPER.md Table 1 (lines 266-272): the paper's direct SL timing on 4 threads (MacBook Pro i7, 2.3 GHz)
+PAPER_TABLE1_4THREADS_S = {32: 1.0, 64: 11.0, 128: 155.0, 256: 2461.0}
+
+
+def run_spheroid(args, rank, world):
+    """PAPER.md Sec. 4.1 / Table 1: one SL evaluation (3-delta extrapolation, rho = (3,4,5),
+    localized) of the Stokeslet integral at the grid points within h outside the translating
+    prolate spheroid; value = pair interactions/s (M N / time); vs_baseline against the
+    paper's own 4-thread time for the same workload; errors vs the exact velocity."""
+    import torch
+
+    import paper_2507_00156_b200 as ser
+    from workloads.spheroid import spheroid_block
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    blk = spheroid_block(args.inv_h)
+    M, N = blk.M, blk.N
+    arrs = ser.to_device(blk, dev)
+    u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    ws = ser.alloc_workspace(M, N, 1, dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        flush.zero_()
+        ser.evaluate(*arrs, blk.h, blk.rho, mode=1, out_u=u, workspace=ws)
+    torch.cuda.synchronize(dev)
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(K):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ser.evaluate(*arrs, blk.h, blk.rho, mode=1, out_u=u, workspace=ws)
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    from paper_2507_00156_b200.sharding import max_over_ranks
+    total_s = max_over_ranks(sum(ms) / 1e3, dev)
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from closed_forms import spheroid_translation_velocity
+    err = np.linalg.norm(u.cpu().numpy() - spheroid_translation_velocity(blk.tgt_xyz), axis=0)
+    value = world * M * N * K / total_s
+    paper_s = PAPER_TABLE1_4THREADS_S.get(args.inv_h)
+    line = {"metric": "Stokeslet (SL) 3-delta extrapolated evaluation on the translating spheroid (PAPER.md Table 1): "
+                      "pair interactions/sec", "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": (value / (M * N / paper_s)) if paper_s else None,
+            "vs_baseline_note": (f"paper's direct sum, 4 threads, {paper_s} s (PAPER.md Table 1, MacBook Pro "
+                                 "2.3 GHz i7): another machine, context") if paper_s else None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": blk.name, "N": N, "M": M, "rho": list(blk.rho), "mode": "SL",
+                       "max_err": float(err.max()), "l2_err": float(np.sqrt((err ** 2).mean())),
+                       "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM"},
+            "clocks": clk.summary(), "gpu_launches": K * ser.launch_count(M, N, 1), "e2e": None}
+    return line
+
+
 def run_twodrop(args, rank, world):
     """NEXT-2 bench: one step = one full GMRES solve of IE (35) (Sec. 4.3)
     on the two drops at 1/h = args.inv_h through stokes_er_twodrop_solve: 4 block
@@ -450,6 +512,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.workload == "spheroid" and args.impl == "ours":
+        line = run_spheroid(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
 
     if args.workload == "tree" and args.impl == "ours":
         line = run_tree(args, rank, world)
