@@ -3,8 +3,9 @@
 //
 //   host   : octree over the sources (stokes_er_tree_build, readings R22)
 //   KW     : modified weights, eq. (32), at the (p+1)^3 second-kind Chebyshev
-//            points of every cluster box (R24), 15 channels: f w, n w (SL) and
-//            q_a n_c w (DL; the DL n w channel is the SL one): leaves from their
+//            points of every cluster box (R24), 12 channels: f w, n w (SL) and the
+//            symmetric part of q_a n_c w (DL: T contracts it with d_a d_c; the DL n w
+//            channel is the SL one): leaves from their
 //            sources (tree_p2m_kernel), internal nodes from their children level by
 //            level (tree_m2m_kernel, separable; exact for degree-p interpolants)
 //   KT     : far part per target: a warp of 32 Morton-consecutive targets walks
@@ -27,7 +28,7 @@
 namespace ser {
 
 constexpr int kTreeMaxDegree = 16;
-constexpr int kTreeCh = 15;               // fw(3) nw(3) q_a n_c w (9)
+constexpr int kTreeCh = 12;               // fw(3) nw(3) symmetric part of q_a n_c w (6)
 constexpr int kTreeStack = 512;           // DFS stack entries per warp (depth <= 63)
 constexpr int kTreeWarps = 4;             // warps per CTA of tree_far_kernel
 #ifndef SER_TREE_MINB
@@ -184,8 +185,18 @@ __global__ void __launch_bounds__(256) tree_p2m_kernel(const TreeNode* __restric
         for (int a = 0; a < 3; ++a) {
           sg[threadIdx.x][a] = s[6 + a];       // f w (0 unless MODE & 1)
           sg[threadIdx.x][3 + a] = s[3 + a];   // n w
-          for (int c = 0; c < 3; ++c) sg[threadIdx.x][6 + 3 * a + c] = (MODE & 2) ? s[9 + a] * s[3 + c] : 0.0;
         }
+        // the DL far term contracts q_a n_c w with d_a d_c only, so its symmetric part
+        // suffices: Q00 Q11 Q22 and Q01+Q10, Q02+Q20, Q12+Q21 (6 channels, not 9)
+        const double* q = s + 9;
+        const double* m = s + 3;
+        const bool dl = MODE & 2;
+        sg[threadIdx.x][6] = dl ? q[0] * m[0] : 0.0;
+        sg[threadIdx.x][7] = dl ? q[1] * m[1] : 0.0;
+        sg[threadIdx.x][8] = dl ? q[2] * m[2] : 0.0;
+        sg[threadIdx.x][9] = dl ? fma(q[0], m[1], q[1] * m[0]) : 0.0;
+        sg[threadIdx.x][10] = dl ? fma(q[0], m[2], q[2] * m[0]) : 0.0;
+        sg[threadIdx.x][11] = dl ? fma(q[1], m[2], q[2] * m[1]) : 0.0;
       }
       __syncthreads();
       if (k < NP)
@@ -276,7 +287,8 @@ struct TreeFarParams {
 struct __align__(16) TreeWarpSmem {
   int stack_node[kTreeStack];
   unsigned stack_mask[kTreeStack];
-  double buf[32][18];     // 32 proxies (coords + 15 channels) or 32 sources (12 doubles)
+  double buf[32][18];     // 32 proxies (coords + 12 channels) or 32 sources (12 doubles); 144-B rows
+                          // (16-B aligned for double2 loads, staggered banks for the per-lane stores)
   double cosk[kTreeMaxDegree + 1];
 };
 
@@ -389,11 +401,10 @@ __global__ void __launch_bounds__(kTreeWarps * 32, SER_TREE_MINB) tree_far_kerne
                 acc.u2 = fma(fma(dz, a3, uz), ri, acc.u2);
               }
               if (MODE & 2) {  // T (eq. 4) on D_ac = G^qn_ac - q0_a G^nw_c (the -6 in the finalize)
-                const double* Q = b + 9;
-                const double w0 = fma(Q[0], dx, fma(Q[1], dy, Q[2] * dz));
-                const double w1 = fma(Q[3], dx, fma(Q[4], dy, Q[5] * dz));
-                const double w2 = fma(Q[6], dx, fma(Q[7], dy, Q[8] * dz));
-                const double dQd = fma(dx, w0, fma(dy, w1, dz * w2));
+                const double* Q = b + 9;  // Q00 Q11 Q22, Q01+Q10, Q02+Q20, Q12+Q21
+                const double w0 = fma(Q[0], dx, fma(Q[3], dy, Q[4] * dz));
+                const double w1 = fma(Q[1], dy, Q[5] * dz);
+                const double dQd = fma(dx, w0, fma(dy, w1, dz * (Q[2] * dz)));
                 const double dq0 = fma(dx, t.q0, fma(dy, t.q1, dz * t.q2));
                 const double dn = fma(dx, b[6], fma(dy, b[7], dz * b[8]));
                 const double c = fma(-dq0, dn, dQd) * (ri2 * ri2 * ri);
