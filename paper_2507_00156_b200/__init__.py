@@ -285,13 +285,12 @@ class TwoDropSolver:
 
 def twodrop_solver(td, device="cuda", max_iter=100, stream=None, tree=None):
     """TwoDropSolver from a workloads.twodrop.TwoDrop input set (numpy arrays -> device)."""
+    import numpy as np
+
     torch = _torch()
-    dev = lambda a: torch.from_numpy(a).to(device)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
     drops = [dict(xyz=dev(d.x), normal=dev(d.n), weight=dev(d.w), f=dev(d.f), lam=d.lam) for d in td.drops]
-    cross = []
-    for c in td.cross:
-        import numpy as np
-        cross.append(dict(b=dev(c.b), x0d=dev(np.ascontiguousarray(np.concatenate([c.n0, c.f0], axis=0)))))
+    cross = [dict(b=dev(c.b), x0d=dev(np.concatenate([c.n0, c.f0], axis=0))) for c in td.cross]
     return TwoDropSolver(drops, cross, td.h, td.rho, td.delta_self, 1.0, td.tol, max_iter, stream, tree)
 
 
