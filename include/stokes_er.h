@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define STOKES_ER_ABI_VERSION 1
+#define STOKES_ER_ABI_VERSION 2  /* 2: options.schedule, NEXT-2 (two drops) and NEXT-3 (treecode) entry points */
 /* c: near iff r <= c * max(delta_k)  ("s1=s2=s3=1 for t > 6") */
 #define STOKES_ER_CUTOFF 6.0
 /* c for the on-surface s# variant: 1 - s2#(6) = 2.45e-12, 1 - s_i#(7) < 1e-16 (R15) */

@@ -699,6 +699,7 @@ const char* stokes_er_status_string(int status) {
     case STOKES_ER_ECUDA: return "CUDA error";
     case STOKES_ER_EWORKSPACE: return "workspace too small";
     case STOKES_ER_EARCH: return "device is not sm_100 (B200)";
+    case STOKES_ER_ENOCONV: return "GMRES reached max_iter above the tolerance";
     default: return "unknown status";
   }
 }
