@@ -147,3 +147,11 @@ def test_twodrop_with_treecode_parity(ser):
     ug, it, _ = s.solve()
     uo, ito, _ = o.solve()
     assert it == ito and rel(ug.cpu().numpy(), uo) <= 1e-8
+
+
+def test_solve_reports_no_convergence(ser):
+    """max_iter below the iterations needed: ENOCONV (include/stokes_er.h), not a silent result."""
+    s = ser.twodrop_solver(twodrop(8), max_iter=3)
+    with pytest.raises(ser._lib.StokesERError) as e:
+        s.solve()
+    assert e.value.status == 5
