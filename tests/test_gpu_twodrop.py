@@ -155,3 +155,28 @@ def test_solve_reports_no_convergence(ser):
     with pytest.raises(ser._lib.StokesERError) as e:
         s.solve()
     assert e.value.status == 5
+
+
+def test_unequal_drop_sizes(ser):
+    """N1 != N2 (drop 2 thinned: not a good quadrature, but the same inputs on both sides):
+    rhs and A u against the oracle."""
+    import torch
+
+    from oracle.twodrop import TwoDropOracle
+    from workloads.twodrop import Cross, Drop, TwoDrop
+
+    td = twodrop(8)
+    d2 = td.drops[1]
+    keep = np.arange(d2.N) % 5 != 0
+    nd2 = Drop(d2.center, np.ascontiguousarray(d2.x[:, keep]), np.ascontiguousarray(d2.n[:, keep]),
+               np.ascontiguousarray(d2.w[keep]), np.ascontiguousarray(d2.f[:, keep]), d2.lam)
+    c1 = td.cross[1]
+    nc1 = Cross(1, 0, np.ascontiguousarray(c1.b[keep]), np.ascontiguousarray(c1.x0[:, keep]),
+                np.ascontiguousarray(c1.n0[:, keep]), np.ascontiguousarray(c1.f0[:, keep]))
+    t2 = TwoDrop(td.h, [td.drops[0], nd2], [td.cross[0], nc1], td.rho, td.delta_self, td.tol, dict(td.meta))
+    assert t2.drops[0].N != t2.drops[1].N
+    o = TwoDropOracle(t2)
+    s = ser.twodrop_solver(t2)
+    assert rel(s.rhs().cpu().numpy(), o.rhs()) <= 1e-12
+    u = np.random.default_rng(5).uniform(-1, 1, t2.n_unknowns)
+    assert rel(s.apply(torch.from_numpy(u).cuda()).cpu().numpy(), o.apply(u)) <= 1e-12
