@@ -338,3 +338,36 @@ def test_target_shards_concatenate(ser):
     us = np.concatenate([p[0] for p in parts], axis=1)
     vs = np.concatenate([p[1] for p in parts], axis=1)
     assert rel(us, u) <= 1e-13 and rel(vs, v) <= 1e-13
+
+
+def test_cuda_graph_capture_and_replay(ser):
+    """stokes_er_eval only enqueues work (no host sync, no allocation), so a whole
+    evaluation can be captured in a CUDA graph and replayed: the replay reproduces the
+    eager result bitwise, also after the inputs change in place."""
+    import torch
+
+    blk = config2(inv_h=16)
+    arrs = ser.to_device(blk)
+    M, N = blk.M, blk.N
+    out_u = torch.empty((3, M), dtype=torch.float64, device="cuda")
+    out_v = torch.empty((3, M), dtype=torch.float64, device="cuda")
+    ws = ser.alloc_workspace(M, N)
+    ref = ser.evaluate(*arrs, blk.h, blk.rho)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up on the side stream (sets kernel attributes)
+        ser.evaluate(*arrs, blk.h, blk.rho, out_u=out_u, out_v=out_v, workspace=ws, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ser.evaluate(*arrs, blk.h, blk.rho, out_u=out_u, out_v=out_v, workspace=ws,
+                     stream=torch.cuda.current_stream())
+    out_u.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out_u, ref[0]) and torch.equal(out_v, ref[1])
+    arrs[3].mul_(2.0)  # f -> 2 f in place (and f(x0) with it): u doubles exactly
+    arrs[7][3:6].mul_(2.0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out_u, 2.0 * ref[0])
