@@ -38,8 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stderr}")
-    with open(os.path.join(PKG, "csrc", "ptxas_report.txt"), "w") as fh:
-        fh.write(res.stderr)
+    with open(os.path.join(PKG, "csrc", "ptxas_report.txt"), "w") as fh:  # registers / spills / smem per kernel
+        fh.write("".join(l for l in res.stderr.splitlines(keepends=True) if "Compile time" not in l))
     if verbose:
         print(res.stderr)
     os.replace(tmp, LIB)
