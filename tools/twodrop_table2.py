@@ -22,7 +22,8 @@ import paper_2507_00156_b200 as ser  # noqa: E402
 from workloads.twodrop import match_nodes, split, twodrop  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
-use_tree = "--tree" in sys.argv  # every block through the treecode with the eq. (33) policy
+use_tree = "--tree" in sys.argv  # every block through the treecode with Table 2's parameters
+gap = next((float(a.split("=")[1]) for a in sys.argv if a.startswith("--xgap=")), None)  # (2+gap, 0, 0) drops
 out_path = args[0] if args else None
 levels = [int(a) for a in args[1:]] or [16, 32, 64, 128]
 
@@ -40,7 +41,7 @@ def policy(inv_h):
 
 rows, sol = [], {}
 for ih in levels:
-    td = twodrop(ih)
+    td = twodrop(ih) if gap is None else twodrop(ih, eps=gap, separation="x")
     t0 = time.perf_counter()
     s = ser.twodrop_solver(td, tree=policy(ih) if use_tree else None)
     torch.cuda.synchronize()
@@ -61,7 +62,7 @@ for ih in levels:
                  "pairs_per_s": pairs_matvec * (it + 1) / (ms / 1e3), "u_max": float(np.abs(u.cpu().numpy()).max())})
     print(rows[-1], flush=True)
 for r, r2 in zip(rows, rows[1:]):
-    tc, uc = sol[r["inv_h"]]
+    tc, uc = sol[r["inv_h"]]  # noqa
     tf, uf = sol[r2["inv_h"]]
     idx = match_nodes(tc, tf)
     c, f = split(tc, uc), split(tf, uf)
@@ -82,7 +83,8 @@ for r, r2 in zip(rows, rows[1:]):
         for rad in (0.1, 0.25, 0.5):
             k = f"max_err_away_{rad}"
             r2[f"order_away_{rad}"] = float(np.log2(r[k] / r2[k]))
-res = {"what": "PAPER.md Table 2 on one B200: two-drop IE (35), GMRES tol 1e-10, "
+res = {"geometry": "centres (0,0,0), (2,0,1/16^3) (PAPER.md:339)" if gap is None else f"centres (0,0,0), (2+{gap},0,0)",
+       "what": "PAPER.md Table 2 on one B200: two-drop IE (35), GMRES tol 1e-10, "
                + ("treecode (Table 2 parameters) on every block" if use_tree else "direct (no treecode) sums"),
        "paper_table2": {"16": [13, 3.17e-3, 1.19e-4], "32": [12, 1.07e-4, 6.11e-6], "64": [12, 4.06e-6, 2.11e-7],
                         "128": [12, 1.02e-7, 6.37e-9], "columns": ["iterations", "max err", "L2 err"]},
