@@ -371,3 +371,33 @@ def test_cuda_graph_capture_and_replay(ser):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out_u, 2.0 * ref[0])
+
+
+@pytest.mark.parametrize("scale", [0.01, 8.0])
+def test_degenerate_delta_scales(ser, scale):
+    """delta far below the node spacing (only r = 0 self pairs are near: the far path does
+    everything else) and far above it (every pair is near: the far path skips every
+    sub-tile as all-near and the near units do all the work); against the oracle."""
+    import dataclasses
+
+    blk = config2(inv_h=16)
+    blk = dataclasses.replace(blk, h=blk.h * scale).take_targets(np.arange(0, blk.M, 3))
+    check_block(ser, blk, localized=False)
+
+
+def test_duplicate_and_zero_weight_sources(ser):
+    """Two nodes at the same position with different densities, and zero-weight nodes
+    (the angular cutoff of the quadrature, reading R10), against the oracle."""
+    import dataclasses
+
+    blk = config1(inv_h=8, per_class=4)
+    k = 17
+    cat = lambda a, b: np.ascontiguousarray(np.concatenate([a, b], axis=-1))
+    dup = dataclasses.replace(blk, src_xyz=cat(blk.src_xyz, blk.src_xyz[:, :k]),
+                              src_normal=cat(blk.src_normal, blk.src_normal[:, :k]),
+                              src_weight=cat(blk.src_weight, 0.5 * blk.src_weight[:k]),
+                              f=cat(blk.f, -blk.f[:, :k]), q=cat(blk.q, 2.0 * blk.q[:, :k]))
+    w = dup.src_weight.copy()
+    w[::11] = 0.0
+    dup = dataclasses.replace(dup, src_weight=w)
+    check_block(ser, dup, localized=False)
