@@ -3,7 +3,7 @@
 // (PAPER.md = arXiv 2507.00156; design: DESIGN.md Sec. 4-5).
 //
 // Pipeline of one stokes_er_eval (all on the caller's stream):
-//   K0a bbox_kernel        bounding box of sources and targets (Morton frame)
+//   K0a bbox_kernel        grid-wide bounding box of sources and targets (Morton frame)
 //   K0b morton_kernel      30-bit Morton keys of sources and targets
 //   K0c CUB radix sort     (key, index) pairs for sources, then targets
 //   K0d pack_sources       AoS records x | m w | f w | q (96 B) in Morton order,
@@ -11,15 +11,23 @@
 //                          per-32-source bounding boxes
 //   K0e pack_targets       SoA records y | alpha = f(x0).n0 | q(x0) | n0 | b |
 //                          extrapolation weights w_k (the 3x3 solve, eq. (17))
-//   K1  pair_kernel        the O(MN) sum: persistent CTAs pull (target block,
-//                          source chunk) items; source tiles are staged to SMEM
-//                          by TMA bulk copies (cp.async.bulk + mbarrier, double
-//                          buffered); each thread keeps T targets in registers;
-//                          warp-level box tests send all-far 32-source sub-tiles
-//                          to the lean far loop and mixed ones
-//                          to the per-pair near/far loop (3 deltas in one pass)
-//   K2  finalize_kernel    sums the chunk partials in fixed order, applies
+//   K13 fused_kernel       (default schedule) one persistent kernel whose CTAs take
+//                          from one interleaved queue
+//                          - far items (K1 body, far_item): a target block x a source
+//                            chunk; source tiles staged to SMEM by TMA bulk copies
+//                            (cp.async.bulk + mbarrier, double buffered); T targets
+//                            per thread in registers; warp-level box tests send
+//                            all-far 32-source sub-tiles to the lean pipelined far
+//                            loop, mixed ones to the loop with the
+//                            near pairs masked, and all-near ones nowhere
+//                          - near units (K3 body, near_unit): 32 targets x one phase of
+//                            their mixed sub-tiles; the near pairs (r <= 6 delta_max)
+//                            with the three regularized kernels folded with the
+//                            extrapolation weights
+//   K1  far_kernel / K3 near_kernel   the same bodies as two kernels (separate schedule)
+//   K2  finalize_kernel    sums the partial slots in fixed order, applies
 //                          1/(8pi), -6, chi q(x0) and un-permutes
+// The treecode (NEXT-3) kernels are in treecode.cuh.
 #pragma once
 #include "stokes_er.h"
 
