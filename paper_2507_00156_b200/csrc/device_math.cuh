@@ -117,9 +117,10 @@ __device__ __forceinline__ double rcp_nr(double x) {
 //   s2 = E - (2/sqrt pi) t e^{-t^2},  c23 = s2 - s3 = (2/sqrt pi)(2/3) t^3 e^{-t^2}.
 // Branch-free, no tables; for t < 0.5 it returns finite values the caller discards.
 __device__ __forceinline__ void sfactor_table(double t, const double* __restrict__ /*unused*/, double& E, double& s2,
-                                              double& c23) {
+                                              double& c23, double* e_out = nullptr) {
   const double u = t * t;
   const double e = exp_neg(u);
+  if (e_out) *e_out = e;  // e^{-t^2}, for callers that need it too (the s# factors)
   const double tc = fmin(t, 6.0);  // erfc(t > 6) < 2e-17: E rounds to 1 either way
   const double x = fma(rcp_nr(kErfcxKappa + tc), kErfcxVA, kErfcxVB);
   double p = kErfcxV[kErfcxDeg];
@@ -173,9 +174,9 @@ __device__ __forceinline__ void sharp_weights(double r, double ri, double invd, 
     A5 = f5 * i3 * invd * invd;
     return;
   }
-  double E, s2, c23;
-  sfactor_table(t, tab, E, s2, c23);
-  const double e = exp_neg(t * t) * kInvSqrtPi;  // e^{-t^2}/sqrt(pi)
+  double E, s2, c23, et;
+  sfactor_table(t, tab, E, s2, c23, &et);
+  const double e = et * kInvSqrtPi;  // e^{-t^2}/sqrt(pi), shared with E's evaluation
   const double t2 = t * t, t3 = t2 * t, t5 = t3 * t2;
   const double s1s = fma((2.0 / 3.0) * e, fma(-2.0, t3, 5.0 * t), E);
   const double s2s = fma(-(2.0 / 3.0) * e, fma(4.0, t5, fma(-14.0, t3, 3.0 * t)), E);
