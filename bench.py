@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
     ap.add_argument("--near-phases", type=int, default=0)
+    ap.add_argument("--chunk-tiles", type=int, default=0, help="far item = chunk x 128 sources (0: automatic)")
     ap.add_argument("--workload", choices=["eval", "twodrop", "tree", "spheroid"], default="eval",
                     help="eval: one stokes_er_eval of BASELINE.json config --config (default); "
                          "twodrop: one GMRES solve of the NEXT-2 two-drop IE (35) at 1/h = --inv-h; "
@@ -560,6 +561,8 @@ def main():
         opt.targets_per_thread = args.targets_per_thread
     if args.near_phases:
         opt.near_phases = args.near_phases
+    if args.chunk_tiles:
+        opt.source_chunk_tiles = args.chunk_tiles
     fused = args.schedule != "separate"
     opt.schedule = {"fused": 0, "separate": 1}[args.schedule]
     nbytes = int(ser._lib.load().stokes_er_workspace_bytes_ex(M, N, 3, __import__("ctypes").byref(opt)))
