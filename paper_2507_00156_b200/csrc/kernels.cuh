@@ -306,53 +306,8 @@ struct Acc {
 // Far pair: unregularized Stokeslet (eq. 3) on g = f w - alpha m w and stresslet
 // (eq. 4) on dq = q - q0 contracted with m w; the -6
 // and 1/(8pi) are applied once in the finalize.  41 FP64 instructions (BOTH).
-#ifndef SER_FAR_V2
-#define SER_FAR_V2 0
-#endif
-template <int MODE>
-__device__ __forceinline__ void far_pair(const Src& s, const Tgt& t, Acc& a) {
-  const double dx = t.y0 - s.x, dy = t.y1 - s.y, dz = t.y2 - s.z;
-  const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-  const double ri = rsqrt_nr(r2);
-  const double ri2 = ri * ri;
-#if SER_FAR_V2
-  if (MODE == 3) {
-    // dot products with d interleaved component-wise: consecutive DFMAs share
-    // their first operand (register-reuse friendly)
-    const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
-    const double qx = s.qx - t.q0, qy = s.qy - t.q1, qz = s.qz - t.q2;
-    double pg = dz * gz, pq = dz * qz, pm = dz * s.mz;
-    pg = fma(dy, gy, pg); pq = fma(dy, qy, pq); pm = fma(dy, s.my, pm);
-    pg = fma(dx, gx, pg); pq = fma(dx, qx, pq); pm = fma(dx, s.mx, pm);
-    const double a3 = pg * ri2;
-    const double c = (pq * pm) * (ri2 * ri2 * ri);
-    a.u0 = fma(fma(dx, a3, gx), ri, a.u0);
-    a.u1 = fma(fma(dy, a3, gy), ri, a.u1);
-    a.u2 = fma(fma(dz, a3, gz), ri, a.u2);
-    a.v0 = fma(dx, c, a.v0);
-    a.v1 = fma(dy, c, a.v1);
-    a.v2 = fma(dz, c, a.v2);
-    return;
-  }
-#endif
-  if (MODE & 1) {
-    const double gx = fma(-t.alpha, s.mx, s.fx), gy = fma(-t.alpha, s.my, s.fy), gz = fma(-t.alpha, s.mz, s.fz);
-    const double a3 = fma(dx, gx, fma(dy, gy, dz * gz)) * ri2;
-    a.u0 = fma(fma(dx, a3, gx), ri, a.u0);
-    a.u1 = fma(fma(dy, a3, gy), ri, a.u1);
-    a.u2 = fma(fma(dz, a3, gz), ri, a.u2);
-  }
-  if (MODE & 2) {
-    const double qx = s.qx - t.q0, qy = s.qy - t.q1, qz = s.qz - t.q2;
-    const double dq = fma(dx, qx, fma(dy, qy, dz * qz));
-    const double dm = fma(dx, s.mx, fma(dy, s.my, dz * s.mz));
-    const double c = (dq * dm) * (ri2 * ri2 * ri);
-    a.v0 = fma(dx, c, a.v0);
-    a.v1 = fma(dy, c, a.v1);
-    a.v2 = fma(dz, c, a.v2);
-  }
-}
-
+// The all-far loop runs it split in two halves (far_geo / far_acc below); the
+// mixed sub-tiles run far_pair_masked.
 // far_pair split in two halves for software pipelining (K1's all-far loop):
 // far_geo (d, r^2 and the MUFU + Newton rsqrt: the long dependency chain) of
 // source k+1 is issued before far_acc (the SL/DL contractions) of source k.
