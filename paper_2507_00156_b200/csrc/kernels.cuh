@@ -73,7 +73,6 @@ struct PairParams {
   double rc2;             // (c delta_max)^2: near iff r^2 <= rc2
   double rc2_box;         // conservative bound for sub-tile tests
   double rc2_inner;       // sub-tiles whose farthest pair is within this are all-near (skipped)
-  double r2_tiny;         // (1e-8 delta_1)^2: r -> 0 limits below (R3)
   double inv_delta[3];
 };
 
@@ -85,7 +84,7 @@ struct NearParams {
   int* counter;           // warp work-queue head
   int64_t Mpad, Npad;
   int n_units, phases;    // unit = (32-target group, phase); phase p takes every phases-th mixed sub-tile
-  double rc2, rc2_box, r2_tiny;
+  double rc2, rc2_box;
   double inv_delta[3];
 };
 
@@ -514,10 +513,6 @@ __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) far_kernel(const PairP
 }
 
 // ------------------------------------------------------------ K3: near pairs
-// Target record in SMEM for the near kernel (16 doubles).
-struct NearTgt {
-  double y0, y1, y2, alpha, q0, q1, q2, n0, n1, n2, b, w0, w1, w2, pad0, pad1;
-};
 
 // Near pair (r <= c delta_max): the three regularized kernels folded with the
 // extrapolation weights w_k:

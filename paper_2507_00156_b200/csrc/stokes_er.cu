@@ -309,7 +309,6 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   pp.rc2 = (cutoff * dmax) * (cutoff * dmax);
   pp.rc2_box = pp.rc2 * (1.0 + 1e-9);
   pp.rc2_inner = pp.rc2 * (1.0 - 1e-9);
-  pp.r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
   for (int k = 0; k < 3; ++k) pp.inv_delta[k] = 1.0 / (rho[k] * h);
 
   NearParams np;
@@ -324,7 +323,6 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   np.Npad = P.Npad;
   np.rc2 = pp.rc2;
   np.rc2_box = pp.rc2_box;
-  np.r2_tiny = pp.r2_tiny;
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = pp.inv_delta[k];
 
   int dev = 0, sms = 0;
@@ -488,7 +486,6 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   np.Npad = P.Npad;
   np.rc2 = rc2;
   np.rc2_box = rc2 * (1.0 + 1e-9);
-  np.r2_tiny = (1e-8 * rho[0] * h) * (1e-8 * rho[0] * h);
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = 1.0 / (rho[k] * h);
   {  // one persistent kernel: tree walks of the target groups + the near units
     int occ = 0;
