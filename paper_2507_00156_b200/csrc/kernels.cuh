@@ -584,19 +584,19 @@ __device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, dou
     const double qx = s.qx - tf[NF_Q0][lane], qy = s.qy - tf[NF_Q1][lane], qz = s.qz - tf[NF_Q2][lane];
     const double dq = fma(dx, qx, fma(dy, qy, dz * qz));
     const double dm = fma(dx, s.mx, fma(dy, s.my, dz * s.mz));
-    const double c = dq * dm * A5;
-    // xh = x - x0 = b n0 - (y - x)   (y = x0 + b n0)
-    const double hx = fma(b, n0, -dx), hy = fma(b, n1, -dy), hz = fma(b, n2, -dz);
+    // t1 contracted with dq and mw (eq. (8)) is
+    //   P = n0 (b a c' - (xh.dq) c' - a (xh.mw)) - xh (a c'),   a = n0.dq, c' = n0.mw,
+    // and with xh = x - x0 = b n0 - (y - x) (y = x0 + b n0) it needs no xh:
+    //   P = (y - x) a c' - n0 (2 b a c' - (d.dq) c' - a (d.mw)),
+    // so v = d ((d.dq)(d.mw) A5 + a c' AP) - n0 (2 b a c' - (d.dq) c' - a (d.mw)) AP.
     const double an = fma(n0, qx, fma(n1, qy, n2 * qz));          // n0.dq
     const double cn = fma(n0, s.mx, fma(n1, s.my, n2 * s.mz));    // n0.mw
-    const double dd = fma(hx, qx, fma(hy, qy, hz * qz));          // xh.dq
-    const double e = fma(hx, s.mx, fma(hy, s.my, hz * s.mz));     // xh.mw
     const double ac = an * cn;
-    const double pn = (fma(b, ac, -dd * cn) - an * e) * AP;       // n0 coefficient of t1 contraction
-    const double ph = ac * AP;                                    // xh coefficient (with minus)
-    a.v0 = fma(dx, c, fma(n0, pn, -hx * ph));
-    a.v1 = fma(dy, c, fma(n1, pn, -hy * ph));
-    a.v2 = fma(dz, c, fma(n2, pn, -hz * ph));
+    const double cd = fma(dq * dm, A5, ac * AP);                    // coefficient of d = y - x
+    const double kn = fma(-an, dm, fma(-dq, cn, (2.0 * b) * ac)) * AP;  // minus the coefficient of n0
+    a.v0 = fma(dx, cd, -n0 * kn);
+    a.v1 = fma(dy, cd, -n1 * kn);
+    a.v2 = fma(dz, cd, -n2 * kn);
   }
   return a;
 }
