@@ -55,8 +55,10 @@ def _reg(r, d):
     return s1 / r, s2 / r ** 3, s3 / r ** 5
 
 
-def brute_deltas(block, targets, mode=3):
+def brute_deltas(block, targets, mode=3, cutoff=None):
     """Definition-mode u^dk, v^dk at 50 digits for the listed target indices.
+    With `cutoff`, s1 = s2 = s3 = 1 for r > cutoff * delta_k (PAPER.md:175 per
+    delta, reading R27: the localized sums).
     Returns dict k -> (u list[3][T], v list[3][T]) as mpf."""
     N = block.N
     X = [[mp.mpf(float(block.src_xyz[i, s])) for s in range(N)] for i in range(3)]
@@ -95,7 +97,10 @@ def brute_deltas(block, targets, mode=3):
             xm = sum(xh[c] * m[c] for c in range(3))
             t1c = [b * n0[i] * nq * nm - (xh[i] * nq * nm + n0[i] * xq * nm + n0[i] * nq * xm) for i in range(3)]
             for k, d in enumerate(deltas):
-                if r == 0:
+                if cutoff is not None and r > cutoff * d:
+                    A1, A3, A5 = 1 / r, 1 / r ** 3, 1 / r ** 5
+                    s2ms3_r3 = mp.mpf(0)
+                elif r == 0:
                     A1, A3, A5 = _reg(r, d)
                     s2ms3_r3 = 4 / (3 * SQPI * d ** 3)
                 else:
