@@ -401,3 +401,23 @@ def test_duplicate_and_zero_weight_sources(ser):
     w[::11] = 0.0
     dup = dataclasses.replace(dup, src_weight=w)
     check_block(ser, dup, localized=False)
+
+
+@pytest.mark.parametrize("r_over_h", [5.0, 11.9, 12.03, 17.98, 18.02, 23.9])
+def test_per_delta_cutoff_pairs(ser, r_over_h):
+    """R27 on the GPU, pair by pair: just inside / just past 6 delta_1 and 6 delta_2
+    (rho = (2, 3, 4)), where the exact s-factors differ from 1 by ~4e-14.  The
+    per-delta values match the oracle to rounding (2e-15; the extrapolated ones,
+    which carry the weights w_k, to 1e-14),
+    far tighter than the general parity tolerance."""
+    from pair_blocks import one_pair_block
+
+    blk = one_pair_block(r_over_h)
+    u, v = run_gpu(ser, blk)
+    ur, vr = oracle.evaluate_block(blk, localized=True)
+    assert rel(u, ur) <= 1e-14 and rel(v, vr) <= 1e-14
+    ud, vd = ser.eval_deltas(*ser.to_device(blk), blk.h, blk.rho)
+    udr, vdr = oracle.eval_deltas_block(blk, localized=True)
+    for k in range(3):
+        assert rel(ud[k].cpu().numpy(), udr[k]) <= 2e-15
+        assert rel(vd[k].cpu().numpy(), vdr[k]) <= 2e-15

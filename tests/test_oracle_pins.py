@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import hp  # noqa: E402
+from pair_blocks import one_pair_block
 from closed_forms import (SHEAR_TRACTION, SHEAR_VELOCITY, chi_of_b, sl_rotation, sl_translation)
 from workloads.configs import config1, config2
 from workloads.densities import ConstField, LinearField, RigidField, ZeroField
@@ -212,23 +213,6 @@ def test_localized_equals_definition(oracle_mod):
         assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
 
 
-def _one_pair_block(r_over_h, h=1 / 64, seed=5):
-    """One source at the origin, one target at distance r_over_h * h along a
-    random direction, random densities (a pair-level pin)."""
-    from workloads.configs import Block
-    rng = np.random.default_rng(seed)
-    m = rng.standard_normal(3); m /= np.linalg.norm(m)
-    e = rng.standard_normal(3); e /= np.linalg.norm(e)
-    y = e * r_over_h * h
-    n0 = rng.standard_normal(3); n0 /= np.linalg.norm(n0)
-    b = 0.3 * h
-    col = lambda v: np.ascontiguousarray(np.asarray(v, float).reshape(-1, 1))
-    x0d = np.concatenate([n0, rng.standard_normal(3), rng.standard_normal(3)])
-    return Block(src_xyz=col(np.zeros(3)), src_normal=col(m), src_weight=np.array([0.7]),
-                 f=col(rng.standard_normal(3)), q=col(rng.standard_normal(3)), tgt_xyz=col(y),
-                 tgt_b=np.array([b]), tgt_x0_density=col(x0d), h=h, rho=(2.0, 3.0, 4.0))
-
-
 @pytest.mark.parametrize("r_over_h", [11.0, 12.03, 17.5, 18.02, 23.9])
 def test_per_delta_cutoff_single_pair(oracle_mod, r_over_h):
     """Reading R27 (PAPER.md:175 per delta): a near pair (r <= 6 delta_3) with
@@ -236,7 +220,7 @@ def test_per_delta_cutoff_single_pair(oracle_mod, r_over_h):
     r = 12.03 h is beyond 6 delta_1 only, 18.02 h beyond 6 delta_1 and 6 delta_2.
     Just past the cutoff the exact s-factors differ from 1 by ~4e-14 (s3), far
     above this pin's rounding tolerance, so a missing or shifted per-delta rule fails."""
-    blk = _one_pair_block(r_over_h)
+    blk = one_pair_block(r_over_h)
     ref = hp.brute_deltas(blk, [0], cutoff=6)
     ud, vd = oracle_mod.eval_deltas_block(blk, localized=True)
     for k in range(3):
