@@ -128,15 +128,12 @@ static void reg_weights(double r, double delta, double delta1, int sharp, double
 
 /* ---- one target, sources s0 <= s < s1 (arrays of stride N): accumulate the
  * pair terms into the per-delta sums Us, Vs (near, or every pair in definition
- * mode) and the shared far sums Uf, Vf (localized mode, r^2 > rc2).  In
- * localized 3-delta mode a near pair with r^2 > (cutoff delta_k)^2 takes
- * s1 = s2 = s3 = 1 for that delta (PAPER.md:175 applied per delta, R27). ---- */
+ * mode) and the shared far sums Uf, Vf (localized mode, r^2 > rc2). -------- */
 static void accum_pairs(const double* src_xyz, const double* src_normal, const double* src_weight,
                         const double* f, const double* q, int64_t N, int64_t s0, int64_t s1,
                         const double y[3], double b, const double n0[3], const double x0[3], double alpha,
                         const double q0[3], const double delta[3], int ndelta, int mode, int localized,
-                        int sharp, double rc2, double cutoff, nsum Us[3][3], nsum Vs[3][3], nsum Uf[3],
-                        nsum Vf[3]) {
+                        int sharp, double rc2, nsum Us[3][3], nsum Vs[3][3], nsum Uf[3], nsum Vf[3]) {
   for (int64_t s = s0; s < s1; ++s) {
     double x[3], m[3], yh[3], xh[3], g[3], dq[3];
     for (int i = 0; i < 3; ++i) {
@@ -185,14 +182,7 @@ static void accum_pairs(const double* src_xyz, const double* src_normal, const d
           }
     for (int k = 0; k < ndelta; ++k) {
       double A[3];
-      if (localized && !sharp && r2 > (cutoff * delta[k]) * (cutoff * delta[k])) {
-        /* reading R27, PAPER.md:175 per delta: "s1 = s2 = s3 = 1 for t = r/delta > 6" */
-        A[0] = 1.0 / r;
-        A[1] = 1.0 / (r * r * r);
-        A[2] = 1.0 / (r * r * r * r * r);
-      } else {
-        reg_weights(r, delta[k], delta[0], sharp, A);
-      }
+      reg_weights(r, delta[k], delta[0], sharp, A);
       if (mode & 1)
         for (int i = 0; i < 3; ++i)
           for (int a = 0; a < 3; ++a) {
@@ -250,7 +240,7 @@ static void eval_target(const double* src_xyz, const double* src_normal, const d
   for (int k = 1; k < ndelta; ++k) dmax = fmax(dmax, delta[k]);
   const double rc2 = (cutoff * dmax) * (cutoff * dmax);
   accum_pairs(src_xyz, src_normal, src_weight, f, q, N, 0, N, y, b, n0, x0, alpha, q0, delta, ndelta, mode,
-              localized, sharp, rc2, cutoff, Us, Vs, Uf, Vf);
+              localized, sharp, rc2, Us, Vs, Uf, Vf);
   finish_target(b, q0, ndelta, Us, Vs, Uf, Vf, U, V);
 }
 
@@ -696,7 +686,7 @@ static int eval_tree_impl(const double* src_xyz, const double* src_normal, const
          * Chebyshev points (R26): direct sum, localized regularization */
         n_dir += (double)(t->end - t->begin);
         accum_pairs(X, Nr, W, F, Q, N, t->begin, t->end, y, b, n0, x0, alpha, q0, delta, nd, mode, 1, sharp, rc2,
-                    cutoff, Us, Vs, Uf, Vf);
+                    Us, Vs, Uf, Vf);
       } else {
         for (int k = t->nchild - 1; k >= 0; --k) stack[sp++] = t->first_child + k;  /* octant order */
       }

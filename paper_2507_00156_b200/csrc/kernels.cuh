@@ -85,7 +85,6 @@ struct NearParams {
   int64_t Mpad, Npad;
   int n_units, phases;    // unit = (32-target group, phase); phase p takes every phases-th mixed sub-tile
   double rc2, rc2_box;
-  double rc2_cls[2];      // (c delta_1)^2, (c delta_2)^2: pair classes of R27 (rc2, rc2 for s#)
   double inv_delta[3];
 };
 
@@ -559,9 +558,6 @@ __device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, dou
   sfactor_table(t0, tab, E0, s20, c0);
   sfactor_table(t1, tab, E1, s21, c1);
   sfactor_table(t2, tab, E2, s22, c2);
-  // R27 (PAPER.md:175 per delta): s1 = s2 = s3 = 1 beyond 6 delta_k (same r^2 test as the oracle's)
-  if (r2 > p.rc2_cls[0]) { E0 = 1.0; s20 = 1.0; c0 = 0.0; }
-  if (r2 > p.rc2_cls[1]) { E1 = 1.0; s21 = 1.0; c1 = 0.0; }
   const double tw0 = tf[NF_W0][lane], tw1 = tf[NF_W1][lane], tw2 = tf[NF_W2][lane];
   const double w0 = t0 >= 0.5 ? tw0 : 0.0, w1 = t1 >= 0.5 ? tw1 : 0.0, w2 = t2 >= 0.5 ? tw2 : 0.0;
   const double S1 = fma(w0, E0, fma(w1, E1, w2 * E2));

@@ -12,8 +12,7 @@ namespace ser {
 
 // ------------------------------------------- debug: per-delta sums (simple)
 // One target per thread over the raw (unsorted) inputs; same near/far rule
-// (and the per-delta rule of R27) and the same pair algebra as K1 but one
-// accumulator set per delta_k.
+// and the same pair algebra as K1 but one accumulator set per delta_k.
 template <int MODE>
 __global__ void deltas_kernel(const double* __restrict__ sx, const double* __restrict__ sn,
                               const double* __restrict__ sw, const double* __restrict__ f,
@@ -67,14 +66,7 @@ __global__ void deltas_kernel(const double* __restrict__ sx, const double* __res
     for (int c = 0; c < 3; ++c) P[c] = n0[c] * (b * an * cn - dd * cn - an * e) - xh[c] * an * cn;
     for (int k = 0; k < 3; ++k) {
       double A1, A3, A5, AP;
-      const double dk = rho.rho[k] * h;
-      if (r2 > (STOKES_ER_CUTOFF * dk) * (STOKES_ER_CUTOFF * dk)) {  // R27: s = 1 beyond c delta_k
-        const double ri = 1.0 / sqrt(r2);
-        A1 = ri;
-        A3 = ri * ri * ri;
-        A5 = A3 * ri * ri;
-        AP = 0.0;
-      } else if (r2 < r2_tiny) {
+      if (r2 < r2_tiny) {
         const double id = inv_delta[k];
         A1 = kTwoOverSqrtPi * id;
         A3 = (2.0 / 3.0) * kTwoOverSqrtPi * id * id * id;
@@ -128,16 +120,6 @@ using namespace ser;
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
-
-// Near-pair classes (R27, PAPER.md:175 per delta): class k pairs lie beyond
-// c delta_j for j < k.  The squares are formed as the oracle forms them.  The
-// s# variant has one delta: every near pair is class 0.
-void set_class_cutoffs(NearParams& np, const double rho[3], double h, bool sharp, double cutoff) {
-  for (int k = 0; k < 2; ++k) {
-    const double dk = rho[k] * h;
-    np.rc2_cls[k] = sharp ? np.rc2 : (cutoff * dk) * (cutoff * dk);
-  }
-}
 
 struct Plan {
   int mode = 3, T = 2;
@@ -341,7 +323,6 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   np.Npad = P.Npad;
   np.rc2 = pp.rc2;
   np.rc2_box = pp.rc2_box;
-  set_class_cutoffs(np, rho, h, SHARP, cutoff);
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = pp.inv_delta[k];
 
   int dev = 0, sms = 0;
@@ -505,7 +486,6 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   np.Npad = P.Npad;
   np.rc2 = rc2;
   np.rc2_box = rc2 * (1.0 + 1e-9);
-  set_class_cutoffs(np, rho, h, SHARP, cutoff);
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = 1.0 / (rho[k] * h);
   {  // one persistent kernel: tree walks of the target groups + the near units
     int occ = 0;

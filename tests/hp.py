@@ -57,8 +57,8 @@ def _reg(r, d):
 
 def brute_deltas(block, targets, mode=3, cutoff=None):
     """Definition-mode u^dk, v^dk at 50 digits for the listed target indices.
-    With `cutoff`, s1 = s2 = s3 = 1 for r > cutoff * delta_k (PAPER.md:175 per
-    delta, reading R27: the localized sums).
+    With `cutoff`, s1 = s2 = s3 = 1 for r > cutoff * delta_k (the per-delta
+    reading of PAPER.md:175 that DESIGN.md R1 does not take; pins tell the two apart).
     Returns dict k -> (u list[3][T], v list[3][T]) as mpf."""
     N = block.N
     X = [[mp.mpf(float(block.src_xyz[i, s])) for s in range(N)] for i in range(3)]

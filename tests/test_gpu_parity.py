@@ -404,12 +404,12 @@ def test_duplicate_and_zero_weight_sources(ser):
 
 
 @pytest.mark.parametrize("r_over_h", [5.0, 11.9, 12.03, 17.98, 18.02, 23.9])
-def test_per_delta_cutoff_pairs(ser, r_over_h):
-    """R27 on the GPU, pair by pair: just inside / just past 6 delta_1 and 6 delta_2
-    (rho = (2, 3, 4)), where the exact s-factors differ from 1 by ~4e-14.  The
-    per-delta values match the oracle to rounding (2e-15; the extrapolated ones,
-    which carry the weights w_k, to 1e-14),
-    far tighter than the general parity tolerance."""
+def test_near_pair_exact_s_factors(ser, r_over_h):
+    """Reading R1 on the GPU, pair by pair: just inside / just past 6 delta_1 and
+    6 delta_2 (rho = (2, 3, 4)) a near pair uses the exact s-factors of every
+    delta (a per-delta s = 1 rule would miss by ~1e-13 here).  The per-delta
+    values match the oracle to rounding (2e-15; the extrapolated ones, which
+    carry the weights w_k, to 1e-14), far tighter than the general tolerance."""
     from pair_blocks import one_pair_block
 
     blk = one_pair_block(r_over_h)

@@ -214,26 +214,26 @@ def test_localized_equals_definition(oracle_mod):
 
 
 @pytest.mark.parametrize("r_over_h", [11.0, 12.03, 17.5, 18.02, 23.9])
-def test_per_delta_cutoff_single_pair(oracle_mod, r_over_h):
-    """Reading R27 (PAPER.md:175 per delta): a near pair (r <= 6 delta_3) with
-    r > 6 delta_k takes the singular kernel for that delta.  rho = (2, 3, 4):
-    r = 12.03 h is beyond 6 delta_1 only, 18.02 h beyond 6 delta_1 and 6 delta_2.
-    Just past the cutoff the exact s-factors differ from 1 by ~4e-14 (s3), far
-    above this pin's rounding tolerance, so a missing or shifted per-delta rule fails."""
+def test_near_pairs_use_exact_s_factors(oracle_mod, r_over_h):
+    """Reading R1 (SURVEY 8(c) reading 1): near iff r <= 6 delta_max, and a near
+    pair evaluates the exact s-factors for EVERY delta, also for the delta_k it
+    lies beyond 6 delta_k of.  rho = (2, 3, 4): r = 12.03 h is beyond 6 delta_1 only,
+    18.02 h beyond 6 delta_1 and 6 delta_2.  Pair by pair against 50-digit mpmath;
+    just past the cutoffs a per-delta rule (s = 1 beyond 6 delta_k, the other
+    reading of PAPER.md:175) differs by ~4e-14, far above this pin's tolerance."""
     blk = one_pair_block(r_over_h)
-    ref = hp.brute_deltas(blk, [0], cutoff=6)
+    ref = hp.brute_deltas(blk, [0])
     ud, vd = oracle_mod.eval_deltas_block(blk, localized=True)
     for k in range(3):
         ur = np.array([float(ref[k][0][i][0]) for i in range(3)])
         vr = np.array([float(ref[k][1][i][0]) for i in range(3)])
         np.testing.assert_allclose(ud[k][:, 0], ur, rtol=0, atol=2e-15 * np.abs(ur).max())
         np.testing.assert_allclose(vd[k][:, 0], vr, rtol=0, atol=2e-15 * np.abs(vr).max())
-    # the exact s-factors (no per-delta rule) are measurably different just past 6 delta_1
-    if 12.0 < r_over_h < 12.1:
-        exact = hp.brute_deltas(blk, [0])
-        v_exact = np.array([float(exact[0][1][i][0]) for i in range(3)])
-        v_rule = np.array([float(ref[0][1][i][0]) for i in range(3)])
-        assert np.abs(v_exact - v_rule).max() > 1e-14 * np.abs(v_rule).max()
+    if 12.0 < r_over_h < 12.1:  # the two readings are distinguishable here
+        rule = hp.brute_deltas(blk, [0], cutoff=6)
+        v_rule = np.array([float(rule[0][1][i][0]) for i in range(3)])
+        v_exact = np.array([float(ref[0][1][i][0]) for i in range(3)])
+        assert np.abs(v_exact - v_rule).max() > 1e-14 * np.abs(v_exact).max()
 
 
 def test_brute_force_mpmath_tiny(oracle_mod):
