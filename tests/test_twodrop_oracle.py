@@ -56,16 +56,20 @@ def test_jump_force_by_hand():
 
 
 def test_twodrop_geometry(td8):
-    """Centres (0,0,0) and (2,0,1/16^3); every node of one drop is
-    outside the other (b' > 0) and y = x0 + b' n0 with x0 on the other sphere."""
+    """Centres (0,0,0) and (2 + 1/16^3, 0, 0) (R17); every node
+    of one drop is outside the other (b' > 0) and y = x0 + b' n0 with x0 on the other
+    sphere; the literal (2, 0, 1/16^3) is separation "z"."""
     for b in range(2):
         cr = td8.cross[b]
         assert cr.b.min() > 0.0
         m = td8.drops[cr.src]
         np.testing.assert_allclose(np.linalg.norm(cr.x0 - m.center[:, None], axis=0), 1.0, atol=1e-14)
         np.testing.assert_allclose(cr.x0 + cr.b * cr.n0, td8.drops[b].x, atol=1e-14)
-    gap = np.sqrt(4.0 + EPS_PAPER ** 2) - 2.0
-    assert min(c.b.min() for c in td8.cross) >= gap - 1e-15
+    np.testing.assert_array_equal(td8.drops[1].center, [2.0 + EPS_PAPER, 0.0, 0.0])
+    assert min(c.b.min() for c in td8.cross) >= EPS_PAPER - 1e-15
+    lit = twodrop(8, separation="z")
+    np.testing.assert_array_equal(lit.drops[1].center, [2.0, 0.0, EPS_PAPER])
+    assert min(c.b.min() for c in lit.cross) >= np.sqrt(4.0 + EPS_PAPER ** 2) - 2.0 - 1e-15
 
 
 def test_interp_reproduces_tangent_polynomials(td8):

@@ -24,6 +24,7 @@ from workloads.twodrop import match_nodes, split, twodrop  # noqa: E402
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 use_tree = "--tree" in sys.argv  # every block through the treecode with Table 2's parameters
 gap = next((float(a.split("=")[1]) for a in sys.argv if a.startswith("--xgap=")), None)  # (2+gap, 0, 0) drops
+literal = "--literal" in sys.argv  # PAPER.md:339 as printed: centres (0,0,0), (2,0,1/16^3)
 out_path = args[0] if args else None
 levels = [int(a) for a in args[1:]] or [16, 32, 64, 128]
 
@@ -41,7 +42,10 @@ def policy(inv_h):
 
 rows, sol = [], {}
 for ih in levels:
-    td = twodrop(ih) if gap is None else twodrop(ih, eps=gap, separation="x")
+    if literal:
+        td = twodrop(ih, separation="z")
+    else:
+        td = twodrop(ih) if gap is None else twodrop(ih, eps=gap, separation="x")
     t0 = time.perf_counter()
     s = ser.twodrop_solver(td, tree=policy(ih) if use_tree else None)
     torch.cuda.synchronize()
@@ -83,7 +87,9 @@ for r, r2 in zip(rows, rows[1:]):
         for rad in (0.1, 0.25, 0.5):
             k = f"max_err_away_{rad}"
             r2[f"order_away_{rad}"] = float(np.log2(r[k] / r2[k]))
-res = {"geometry": "centres (0,0,0), (2,0,1/16^3) (PAPER.md:339)" if gap is None else f"centres (0,0,0), (2+{gap},0,0)",
+c2 = [float(v) for v in sol[levels[0]][0].drops[1].center]
+res = {"geometry": f"centres (0,0,0), {tuple(c2)}" + (" (PAPER.md:339 as printed)" if literal else
+                                                     " (separation 2 + eps along x_1, DESIGN.md R17)"),
        "what": "PAPER.md Table 2 on one B200: two-drop IE (35), GMRES tol 1e-10, "
                + ("treecode (Table 2 parameters) on every block" if use_tree else "direct (no treecode) sums"),
        "paper_table2": {"16": [13, 3.17e-3, 1.19e-4], "32": [12, 1.07e-4, 6.11e-6], "64": [12, 4.06e-6, 2.11e-7],

@@ -2,9 +2,11 @@
 
 Geometry and data only -- none of the layer-potential arithmetic lives here.
 
-  * two unit spheres ("drops"), centres c_1 = (0, 0, 0) and c_2 = (2, 0, eps),
-    eps = 1/16^3 (PAPER.md:339 literally; the gap is sqrt(4 + eps^2) - 2 ~ 1.5e-8,
-    DESIGN.md R17), each with its own centre-anchored quadrature grid (PAPER.md:142-160);
+  * two unit spheres ("drops"), centres c_1 = (0, 0, 0) and c_2 = (2 + eps, 0, 0),
+    eps = 1/16^3: SURVEY 8(c) reading 12 of PAPER.md:339 ("centered ... at (2,0,eps)",
+    read as a typo for a centre separation 2 + eps along x_1; R17).  The
+    literal (2, 0, eps) (gap sqrt(4 + eps^2) - 2 ~ 1.5e-8) is separation="z".  Each
+    drop has its own centre-anchored quadrature grid (PAPER.md:142-160);
   * viscosity ratios lambda_1 = lambda_2 = 2, mu_0 = 1 (PAPER.md:337-338);
   * interface force jump [f] = 2 gamma H n - grad_S gamma with gamma = 1 + (x_1 - x_c)^2,
     x_c the centre's x-coordinate, H = 1 (mean curvature of a unit sphere, the average of
@@ -99,11 +101,11 @@ def _c(a):
 
 
 def twodrop(inv_h: int = 16, eps: float = EPS_PAPER, lam=(LAMBDA_PAPER, LAMBDA_PAPER),
-            separation: str = "z") -> TwoDrop:
+            separation: str = "x") -> TwoDrop:
     """The PAPER.md Sec. 4.3 two-drop inputs at grid spacing h = 1/inv_h.
 
-    separation "z": c_2 = (2, 0, eps) (the paper's statement); "x": c_2 = (2 + eps, 0, 0)
-    (a finite gap eps along x_1, as in BASELINE.json config 4)."""
+    separation "x" (default, DESIGN.md R17): c_2 = (2 + eps, 0, 0), a gap eps along x_1;
+    "z": c_2 = (2, 0, eps), PAPER.md:339 taken literally."""
     h = 1.0 / inv_h
     c1 = np.zeros(3)
     c2 = np.array([2.0, 0.0, eps]) if separation == "z" else np.array([2.0 + eps, 0.0, 0.0])
