@@ -484,7 +484,7 @@ def run_twodrop(args, rank, world):
             "config": {"workload": f"twodrop_h1/{args.inv_h}", "N_per_drop": N, "iterations": it,
                        "block_evals_per_solve": 4 * (it + 1), "pairs_per_solve": pairs,
                        "near_pairs_per_solve": int(near), "rho_cross": list(td.rho), "delta_self_over_h": 3.0,
-                       "eps": td.meta["eps"], "lambda": list(td.meta["lambda"]), "tol": td.tol,
+                       "eps": td.meta["eps"], "centre_2": [float(c) for c in td.drops[1].center], "lambda": list(td.meta["lambda"]), "tol": td.tol,
                        "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM",
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
