@@ -58,7 +58,7 @@ constexpr int kSrcDoubles = 12;      // packed source record: x(3) mw(3) fw(3) q
 constexpr int kTgtFields = 14;       // y(3) alpha q0(3) n0(3) b w(3)
 constexpr int kTileBytes = kTile * kSrcDoubles * 8;
 constexpr int kFarSmemBytes = 2 * kTileBytes;  // far-item TMA double buffer
-constexpr double kPartialCapBytes = 256.0 * 1024 * 1024;
+constexpr double kPartialCapBytes = 1024.0 * 1024 * 1024;  // far partial sums (workspace)
 
 enum TgtField { F_Y0 = 0, F_Y1, F_Y2, F_ALPHA, F_Q0, F_Q1, F_Q2, F_N0, F_N1, F_N2, F_B, F_W0, F_W1, F_W2 };
 
