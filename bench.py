@@ -39,6 +39,9 @@ UNIT = "pairs/s"
 F_FAR_ALG = 57
 F_FAR_SL, F_FAR_DL = 35, 33  # SL-only / DL-only far pairs
 F_NEAR_ALG = 180
+# NEXT-1 s# near pair (one delta): y-x 3, r^2 5, rsqrt 1, r 1, t 1, erf 1, exp 1, t^2 t^3 t^5 3,
+# s#1..3 polynomials 18, A1 A3 A5 5, SL 24, DL (unsplit, as the far pair) 21
+F_NEAR_SHARP_ALG = 84
 F_FAR_ISSUED = 64   # ncu-countable FP64 flops (2*DFMA + DMUL + DADD) of far_pair<3> (41 instructions)
 F_NEAR_ISSUED = 378  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r01/ncu_full_v8: 144 DFMA, 60 DMUL, 30 DADD)
 SMS = 148
@@ -58,8 +61,10 @@ def parse():
     ap.add_argument("--targets-per-thread", type=int, default=0)
     ap.add_argument("--near-phases", type=int, default=0)
     ap.add_argument("--chunk-tiles", type=int, default=0, help="far item = chunk x 128 sources (0: automatic)")
-    ap.add_argument("--workload", choices=["eval", "twodrop", "tree", "spheroid"], default="eval",
+    ap.add_argument("--workload", choices=["eval", "twodrop", "tree", "spheroid", "onsurface"], default="eval",
                     help="eval: one stokes_er_eval of BASELINE.json config --config (default); "
+                         "onsurface: one stokes_er_eval_onsurface (NEXT-1, s#, delta = 3h) of config 5 "
+                         "(every node a target) at 1/h = --inv-h; "
                          "twodrop: one GMRES solve of the NEXT-2 two-drop IE (35) at 1/h = --inv-h; "
                          "tree: one stokes_er_eval_tree (NEXT-3) of config --config at 1/h = --inv-h; "
                          "spheroid: PAPER.md Table 1's SL evaluation at 1/h = --inv-h")
@@ -323,6 +328,84 @@ def run_tree(args, rank, world):
     return line
 
 
+def run_onsurface(args, rank, world):
+    """NEXT-1 bench: one step = one stokes_er_eval_onsurface (s# factors, one delta = 3h, cutoff 7;
+    PAPER.md:126-139 and 341) of config 5 (M = N: every sphere node is a target, b = 0) at
+    1/h = --inv-h; value = pair interactions per second (M N / time)."""
+    import torch
+    from scipy.spatial import cKDTree
+
+    import paper_2507_00156_b200 as ser
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    block = make_workload(5, args.inv_h, rank)
+    M, N = block.M, block.N
+    delta = 3.0 * block.h
+    arrs = ser.to_device(block, dev)
+    u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    v = torch.empty((3, M), dtype=torch.float64, device=dev)
+    ws = ser.alloc_workspace(M, N, 3, dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        flush.zero_()
+        ser.evaluate_onsurface(*arrs, delta, out_u=u, out_v=v, workspace=ws)
+    torch.cuda.synchronize(dev)
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(K):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ser.evaluate_onsurface(*arrs, delta, out_u=u, out_v=v, workspace=ws)
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    from paper_2507_00156_b200.sharding import max_over_ranks
+    total_s = max_over_ranks(sum(ms) / 1e3, dev)
+    if rank != 0:
+        return None
+    near = int(cKDTree(block.tgt_xyz.T).count_neighbors(cKDTree(block.src_xyz.T), 7.0 * delta))
+    flops = (M * N - near) * F_FAR_ALG + near * F_NEAR_SHARP_ALG
+    peak = SMS * FP64_LANES_PER_SM * 2 * 1965.0 * 1e6 / 1e12
+    achieved = flops / (total_s / K) / 1e12
+    line = {"metric": "on-surface s# (NEXT-1) SL+DL evaluation: target-source pair interactions/sec",
+            "value": world * M * N * K / total_s, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": block.name + "_onsurface", "N": N, "M": M, "delta_over_h": 3.0, "cutoff": 7.0,
+                       "near_pairs_per_step": near, "l2": "flushed between timed steps (256 MiB write)",
+                       "inputs": "resident in HBM"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": f"the whole evaluation: {F_FAR_ALG} flops per far pair, {F_NEAR_SHARP_ALG} per "
+                                   "s# near pair (rsqrt, erf, exp = 1)",
+                         "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz"},
+            "clocks": clk.summary(), "gpu_launches": K * 7,
+            "gpu_launches_note": "per step: bbox, 2 morton, pack sources, pack targets, fused far+near, finalize "
+                                 "(+ CUB sort)",
+            "e2e": None}
+    if not args.no_cpu_baseline:  # the oracle's sharp mode on a target sample, host cores
+        import oracle
+        rng = np.random.default_rng(0)
+        k = max(64, min(M, int(2e9 / N)))
+        idx = np.sort(rng.choice(M, min(M, k), replace=False))
+        sub = block.take_targets(idx)
+        t0 = time.perf_counter()
+        ur, vr = oracle.evaluate_sharp(*sub.arrays(), delta, localized=True, cutoff=7.0)
+        dt = time.perf_counter() - t0
+        uu, vv = u.cpu().numpy()[:, idx], v.cpu().numpy()[:, idx]
+        line["config"]["max_rel_diff_vs_oracle_sample"] = max(float(np.abs(uu - ur).max() / np.abs(ur).max()),
+                                                              float(np.abs(vv - vr).max() / np.abs(vr).max()))
+        line["cpu_baseline"] = {"value": len(idx) * N / dt, "unit": UNIT, "cores": oracle.max_threads(),
+                                "kind": "oracle",
+                                "sample": f"{len(idx)} random targets of {M} x all {N} sources, sharp mode, "
+                                          f"localized, {dt:.1f} s wall"}
+    return line
+
+
 # PAPER.md Table 1 (lines 266-272): the paper's direct SL timing on 4 threads (MacBook Pro i7, 2.3 GHz)
 PAPER_TABLE1_4THREADS_S = {32: 1.0, 64: 11.0, 128: 155.0, 256: 2461.0}
 
@@ -522,6 +605,12 @@ def main():
 
     if args.workload == "tree" and args.impl == "ours":
         line = run_tree(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    if args.workload == "onsurface" and args.impl == "ours":
+        line = run_onsurface(args, rank, world)
         if line is not None:
             print(json.dumps(line), flush=True)
         return
