@@ -42,7 +42,7 @@
 namespace ser {
 
 #ifndef SER_FAR_THREADS
-#define SER_FAR_THREADS 128
+#define SER_FAR_THREADS 64
 #endif
 constexpr int kThreads = SER_FAR_THREADS;  // threads per far-kernel CTA (tuning macro)
 #ifndef SER_FAR_UNROLL
@@ -622,7 +622,7 @@ __device__ __forceinline__ Src load_src_global(const double* __restrict__ g) {
 // near sources to a per-lane ring queue in SMEM.  Whenever every lane holds
 // work, all lanes evaluate one queued pair each per round (no divergence); a
 // lane's pairs are added in discovery order: deterministic.
-constexpr int kNearWarps = 4;
+constexpr int kNearWarps = SER_FAR_THREADS / 32;  // one near unit per warp of the fused CTA
 constexpr int kQCap = 64;  // per-lane ring capacity (power of two)
 #ifndef SER_NEAR_MINB
 #define SER_NEAR_MINB 4
