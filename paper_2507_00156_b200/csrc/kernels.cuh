@@ -523,11 +523,16 @@ __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) far_kernel(const PairP
 //       eq. 7 rearranged: T1 s2 + T2 s3 = -6[yyy s3/r^5 + t1 (s2-s3)/r^3])
 // Target fields other than y live in SMEM, SoA [field][lane] (conflict-free).
 enum NearField { NF_ALPHA = 0, NF_Q0, NF_Q1, NF_Q2, NF_N0, NF_N1, NF_N2, NF_B, NF_W0, NF_W1, NF_W2, kNearFields };
+// The near accumulators of one target: u, the d-part of v, and kn, the sum of
+// the n0 coefficients (n0 is the target's, so sum_pairs n0 kn = n0 sum kn:
+// v = (v0, v1, v2) - n0 kn at the end).  Each pair adds with fused FMAs.
+struct NearAcc {
+  double u0, u1, u2, v0, v1, v2, kn;
+};
 template <int MODE, bool SHARP>
-__device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, double y2,
-                                         const double (*__restrict__ tf)[32], int lane, const NearParams& p,
-                                         const double* __restrict__ tab) {
-  Acc a{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+__device__ __forceinline__ void near_pair(const Src& s, double y0, double y1, double y2,
+                                          const double (*__restrict__ tf)[32], int lane, const NearParams& p,
+                                          const double* __restrict__ tab, NearAcc& a) {
   const double dx = y0 - s.x, dy = y1 - s.y, dz = y2 - s.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   const double ri = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;
@@ -539,18 +544,18 @@ __device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, dou
       const double alpha = tf[NF_ALPHA][lane];
       const double gx = fma(-alpha, s.mx, s.fx), gy = fma(-alpha, s.my, s.fy), gz = fma(-alpha, s.mz, s.fz);
       const double dg = fma(dx, gx, fma(dy, gy, dz * gz)) * A3;
-      a.u0 = fma(gx, A1, dx * dg);
-      a.u1 = fma(gy, A1, dy * dg);
-      a.u2 = fma(gz, A1, dz * dg);
+      a.u0 = fma(gx, A1, fma(dx, dg, a.u0));
+      a.u1 = fma(gy, A1, fma(dy, dg, a.u1));
+      a.u2 = fma(gz, A1, fma(dz, dg, a.u2));
     }
     if (MODE & 2) {
       const double qx = s.qx - tf[NF_Q0][lane], qy = s.qy - tf[NF_Q1][lane], qz = s.qz - tf[NF_Q2][lane];
       const double c = fma(dx, qx, fma(dy, qy, dz * qz)) * fma(dx, s.mx, fma(dy, s.my, dz * s.mz)) * A5;
-      a.v0 = dx * c;
-      a.v1 = dy * c;
-      a.v2 = dz * c;
+      a.v0 = fma(dx, c, a.v0);
+      a.v1 = fma(dy, c, a.v1);
+      a.v2 = fma(dz, c, a.v2);
     }
-    return a;
+    return;
   }
   // all three deltas through the branch-free table path (independent chains)
   const double t0 = r * p.inv_delta[0], t1 = r * p.inv_delta[1], t2 = r * p.inv_delta[2];
@@ -575,9 +580,9 @@ __device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, dou
     const double alpha = tf[NF_ALPHA][lane];
     const double gx = fma(-alpha, s.mx, s.fx), gy = fma(-alpha, s.my, s.fy), gz = fma(-alpha, s.mz, s.fz);
     const double dg = fma(dx, gx, fma(dy, gy, dz * gz)) * A3;
-    a.u0 = fma(gx, A1, dx * dg);
-    a.u1 = fma(gy, A1, dy * dg);
-    a.u2 = fma(gz, A1, dz * dg);
+    a.u0 = fma(gx, A1, fma(dx, dg, a.u0));
+    a.u1 = fma(gy, A1, fma(dy, dg, a.u1));
+    a.u2 = fma(gz, A1, fma(dz, dg, a.u2));
   }
   if (MODE & 2) {
     const double n0 = tf[NF_N0][lane], n1 = tf[NF_N1][lane], n2 = tf[NF_N2][lane], b = tf[NF_B][lane];
@@ -588,17 +593,17 @@ __device__ __forceinline__ Acc near_pair(const Src& s, double y0, double y1, dou
     //   P = n0 (b a c' - (xh.dq) c' - a (xh.mw)) - xh (a c'),   a = n0.dq, c' = n0.mw,
     // and with xh = x - x0 = b n0 - (y - x) (y = x0 + b n0) it needs no xh:
     //   P = (y - x) a c' - n0 (2 b a c' - (d.dq) c' - a (d.mw)),
-    // so v = d ((d.dq)(d.mw) A5 + a c' AP) - n0 (2 b a c' - (d.dq) c' - a (d.mw)) AP.
+    // so v = d ((d.dq)(d.mw) A5 + a c' AP) - n0 (2 b a c' - (d.dq) c' - a (d.mw)) AP; the n0 term is
+    // summed as a scalar (NearAcc::kn) and applied once per target.
     const double an = fma(n0, qx, fma(n1, qy, n2 * qz));          // n0.dq
     const double cn = fma(n0, s.mx, fma(n1, s.my, n2 * s.mz));    // n0.mw
     const double ac = an * cn;
     const double cd = fma(dq * dm, A5, ac * AP);                    // coefficient of d = y - x
-    const double kn = fma(-an, dm, fma(-dq, cn, (2.0 * b) * ac)) * AP;  // minus the coefficient of n0
-    a.v0 = fma(dx, cd, -n0 * kn);
-    a.v1 = fma(dy, cd, -n1 * kn);
-    a.v2 = fma(dz, cd, -n2 * kn);
+    a.kn = fma(fma(-an, dm, fma(-dq, cn, (2.0 * b) * ac)), AP, a.kn);  // minus the coefficient of n0
+    a.v0 = fma(dx, cd, a.v0);
+    a.v1 = fma(dy, cd, a.v1);
+    a.v2 = fma(dz, cd, a.v2);
   }
-  return a;
 }
 
 template <int MODE>
@@ -625,7 +630,7 @@ __device__ __forceinline__ Src load_src_global(const double* __restrict__ g) {
 constexpr int kNearWarps = SER_FAR_THREADS / 32;  // one near unit per warp of the fused CTA
 constexpr int kQCap = 64;  // per-lane ring capacity (power of two)
 #ifndef SER_NEAR_MINB
-#define SER_NEAR_MINB 4
+#define SER_NEAR_MINB (512 / SER_FAR_THREADS)  // 16 resident warps per SM
 #endif
 // Per-warp SMEM of the near unit: source xyz of the sub-tile being classified,
 // the per-lane ring queues and the lane targets' fields (SoA [field][lane]).
@@ -667,7 +672,7 @@ __device__ __forceinline__ void near_unit(const NearParams& p, int unit, NearSme
       lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
       hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
     }
-  Acc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  NearAcc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int head = 0, tail = 0;
   int ordinal = 0;  // index of the mixed sub-tile among this group's mixed sub-tiles
 
@@ -738,17 +743,17 @@ __device__ __forceinline__ void near_unit(const NearParams& p, int unit, NearSme
         const int sidx = q[head & (kQCap - 1)][lane];
         ++head;
         const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
-        const Acc d = near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, nullptr);
-        acc.u0 += d.u0; acc.u1 += d.u1; acc.u2 += d.u2;
-        acc.v0 += d.v0; acc.v1 += d.v1; acc.v2 += d.v2;
+        near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, nullptr, acc);
       }
     }
     if (last) break;
   }
+  const double v0 = fma(-tf[NF_N0][lane], acc.kn, acc.v0), v1 = fma(-tf[NF_N1][lane], acc.kn, acc.v1),
+               v2 = fma(-tf[NF_N2][lane], acc.kn, acc.v2);
   __syncwarp();  // all lanes done with sm before the warp's next unit overwrites it
   double* out = p.near_out + (int64_t)phase * 6 * p.Mpad + ti;
   out[0 * p.Mpad] = acc.u0; out[1 * p.Mpad] = acc.u1; out[2 * p.Mpad] = acc.u2;
-  out[3 * p.Mpad] = acc.v0; out[4 * p.Mpad] = acc.v1; out[5 * p.Mpad] = acc.v2;
+  out[3 * p.Mpad] = v0; out[4 * p.Mpad] = v1; out[5 * p.Mpad] = v2;
 }
 
 // K3 (separate schedule): persistent warps pull units (group, phase) from a
