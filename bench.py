@@ -43,7 +43,7 @@ F_NEAR_ALG = 180
 # s#1..3 polynomials 18, A1 A3 A5 5, SL 24, DL (unsplit, as the far pair) 21
 F_NEAR_SHARP_ALG = 84
 F_FAR_ISSUED = 64   # ncu-countable FP64 flops (2*DFMA + DMUL + DADD) of far_pair<3> (41 instructions)
-F_NEAR_ISSUED = 378  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r01/ncu_full_v8: 144 DFMA, 60 DMUL, 30 DADD)
+F_NEAR_ISSUED = 343  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r01/ncu_full_v15_far_near.json: 135 DFMA, 48 DMUL, 24 DADD)
 SMS = 148
 FP64_LANES_PER_SM = 64  # measured: DFMA loop 58.7 FMA/clk/SM at the boost clock (tools/probes)
 

@@ -45,6 +45,15 @@ def main(rep, out):
                         k.setdefault("stalls_per_issue", {})[name[len(STALL_PREFIX):-len("_per_issue_active.ratio")]] = float(v)
                 except ValueError:
                     pass
+        # FP64 op totals: this ncu reports the .sum of the SASS op counters only per elapsed cycle
+        try:
+            cyc = float(row[hdr.index("smsp__cycles_elapsed.avg")])
+            for op in ("dfma", "dmul", "dadd"):
+                name = f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed"
+                if name in hdr and f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum" not in k:
+                    k[f"fp64_{op}_thread_inst_total"] = float(row[hdr.index(name)]) * cyc
+        except (ValueError, IndexError):
+            pass
         res.append(k)
     with open(out, "w") as fh:
         json.dump({"report": rep, "kernels": res}, fh, indent=1)
