@@ -45,6 +45,9 @@ namespace ser {
 #define SER_FAR_THREADS 64
 #endif
 constexpr int kThreads = SER_FAR_THREADS;  // threads per far-kernel CTA (tuning macro)
+#ifndef SER_HALF_BOXES
+#define SER_HALF_BOXES 1  // mixed sub-tiles re-classified by 16-source halves (tuning macro)
+#endif
 #ifndef SER_FAR_UNROLL
 #define SER_FAR_UNROLL 2
 #endif
@@ -64,7 +67,7 @@ enum TgtField { F_Y0 = 0, F_Y1, F_Y2, F_ALPHA, F_Q0, F_Q1, F_Q2, F_N0, F_N1, F_N
 
 struct PairParams {
   const double* src;      // [Npad][12]
-  const double* src_box;  // [Npad/32][8]  lo xyz, pad, hi xyz, pad
+  const double* src_box;  // [Npad/32][8]  lo xyz, pad, hi xyz, pad; then [Npad/16][8] half boxes
   const double* tgt;      // [14][Mpad]
   double* partial;        // [items][6][TB]
   int* counter;           // work-queue head
@@ -223,10 +226,20 @@ __global__ void pack_sources(const double* __restrict__ xyz, const double* __res
   double lo[3] = {rec[0], rec[1], rec[2]}, hi[3] = {rec[0], rec[1], rec[2]};
 #pragma unroll
   for (int d = 0; d < 3; ++d)
-    for (int o = 16; o; o >>= 1) {
+    for (int o = 8; o; o >>= 1) {
       lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
       hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
     }
+  if ((threadIdx.x & 15) == 0) {  // the 16-source half box (after the Npad/32 full boxes)
+    double* b = src_box + (Npad >> 5) * 8 + (i >> 4) * 8;
+    b[0] = lo[0]; b[1] = lo[1]; b[2] = lo[2]; b[3] = 0.0;
+    b[4] = hi[0]; b[5] = hi[1]; b[6] = hi[2]; b[7] = 0.0;
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], 16));
+    hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], 16));
+  }
   if ((threadIdx.x & 31) == 0) {
     double* b = src_box + (i >> 5) * 8;
     b[0] = lo[0]; b[1] = lo[1]; b[2] = lo[2]; b[3] = 0.0;
@@ -370,6 +383,39 @@ __device__ __forceinline__ void far_pair_masked(const Src& s, const Tgt& t, Acc&
   }
 }
 
+// The all-far loop over NS sources at ss (software pipeline: geometry + rsqrt of
+// source k+1 overlap the contractions of source k; the last step recomputes
+// source 0 and discards it).
+template <int MODE, int T, int NS>
+__device__ __forceinline__ void far_run(const double* ss, const Tgt (&tg)[T], Acc (&acc)[T]) {
+  Src s = load_src<MODE>(ss);
+  Geo g[T];
+#pragma unroll
+  for (int j = 0; j < T; ++j) g[j] = far_geo(s, tg[j]);
+#pragma unroll kFarUnroll
+  for (int k = 0; k < NS; ++k) {
+    const Src sn = load_src<MODE>(ss + ((k + 1) & (NS - 1)) * kSrcDoubles);
+    Geo gn[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) gn[j] = far_geo(sn, tg[j]);
+#pragma unroll
+    for (int j = 0; j < T; ++j) far_acc<MODE>(s, tg[j], g[j], acc[j]);
+    s = sn;
+#pragma unroll
+    for (int j = 0; j < T; ++j) g[j] = gn[j];
+  }
+}
+// The mixed loop: far pairs only (near pairs masked, the near kernel owns them).
+template <int MODE, int T, int NS>
+__device__ __forceinline__ void far_run_masked(const double* ss, const Tgt (&tg)[T], Acc (&acc)[T], double rc2) {
+#pragma unroll 2
+  for (int k = 0; k < NS; ++k) {
+    const Src s = load_src<MODE>(ss + k * kSrcDoubles);
+#pragma unroll
+    for (int j = 0; j < T; ++j) far_pair_masked<MODE>(s, tg[j], acc[j], rc2);
+  }
+}
+
 // K1 body: one far work item = (target block of kThreads*T targets, source
 // chunk) -- the far-field pair sums (the non-local part,
 // computed once and shared by the three deltas).  Each item's partial sums go
@@ -445,31 +491,31 @@ __device__ __forceinline__ void far_item(const PairParams& p, int item, double (
       }
       const double* ss = sm + sub * kSub * kSrcDoubles;
       if (g2 > p.rc2_box) {  // warp-uniform: every pair of this sub-tile is far
-        // software pipeline: geometry + rsqrt of source k+1 overlap the
-        // contractions of source k (the last step recomputes source 0: discarded)
-        Src s = load_src<MODE>(ss);
-        Geo g[T];
-#pragma unroll
-        for (int j = 0; j < T; ++j) g[j] = far_geo(s, tg[j]);
-#pragma unroll kFarUnroll
-        for (int k = 0; k < kSub; ++k) {
-          const Src sn = load_src<MODE>(ss + ((k + 1) & (kSub - 1)) * kSrcDoubles);
-          Geo gn[T];
-#pragma unroll
-          for (int j = 0; j < T; ++j) gn[j] = far_geo(sn, tg[j]);
-#pragma unroll
-          for (int j = 0; j < T; ++j) far_acc<MODE>(s, tg[j], g[j], acc[j]);
-          s = sn;
-#pragma unroll
-          for (int j = 0; j < T; ++j) g[j] = gn[j];
-        }
+        far_run<MODE, T, kSub>(ss, tg, acc);
       } else if (f2 > p.rc2_inner) {  // mixed: far pairs only, near pairs belong to the near kernel
-#pragma unroll 2
-        for (int k = 0; k < kSub; ++k) {
-          const Src s = load_src<MODE>(ss + k * kSrcDoubles);
+#if SER_HALF_BOXES
+        // the two 16-source halves are classified again: all-far halves take the
+        // lean loop, all-near ones are skipped, only mixed halves mask pairs
+        const double* hb = p.src_box + (p.n_tiles * (int64_t)kTile / kSub) * 8 +
+                           ((int64_t)(tile0 + t) * (kTile / 16) + sub * 2) * 8;
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          double h2 = 0.0, s2 = 0.0;
 #pragma unroll
-          for (int j = 0; j < T; ++j) far_pair_masked<MODE>(s, tg[j], acc[j], p.rc2);
+          for (int d = 0; d < 3; ++d) {
+            const double blo = __ldg(hb + hf * 8 + d), bhi = __ldg(hb + hf * 8 + 4 + d);
+            const double gap = fmax(0.0, fmax(blo - hi[d], lo[d] - bhi));
+            const double span = fmax(bhi - lo[d], hi[d] - blo);
+            h2 = fma(gap, gap, h2);
+            s2 = fma(span, span, s2);
+          }
+          const double* hs = ss + hf * 16 * kSrcDoubles;
+          if (h2 > p.rc2_box) far_run<MODE, T, 16>(hs, tg, acc);
+          else if (s2 > p.rc2_inner) far_run_masked<MODE, T, 16>(hs, tg, acc, p.rc2);
         }
+#else
+        far_run_masked<MODE, T, kSub>(ss, tg, acc, p.rc2);
+#endif
       }  // else: every pair of the sub-tile is near (r^2 <= rc2): nothing far to add
     }
     far_bar_sync();  // all reads of `buf` done before it is refilled

@@ -180,7 +180,7 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override, int ph
   p.off_tvout = take(M * 4);
   p.off_cub = take(p.cub_bytes);
   p.off_src = take(p.Npad * kSrcDoubles * sizeof(double));
-  p.off_srcbox = take((p.Npad / kSub) * 8 * sizeof(double));
+  p.off_srcbox = take((p.Npad / kSub + p.Npad / 16) * 8 * sizeof(double));  // 32-source boxes, then halves
   p.off_tgt = take(p.Mpad * kTgtFields * sizeof(double));
   p.off_orig = take(p.Mpad * sizeof(int32_t));
   p.off_partial = take((size_t)p.n_items * 6 * TB * sizeof(double));
