@@ -215,7 +215,7 @@ def cpu_baseline(block):
 def committed_traffic(fused: bool):
     """DRAM bytes (read + write) per launch of the dominant kernel from the committed
     `ncu --set full` summary of this bench command (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_v15_fused.json")
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_v16_fused.json")
     if not fused or not os.path.exists(path):
         return None
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -225,7 +225,7 @@ def committed_traffic(fused: bool):
             for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 v, u = k[key].split()
                 tot += float(v) * units[u]
-            return int(tot), "profiles/r01/ncu_full_v15_fused.json (one ncu --set full capture of this command)"
+            return int(tot), "profiles/r01/ncu_full_v16_fused.json (one ncu --set full capture of this command)"
     return None
 
 def twodrop_launches(it: int) -> int:
