@@ -421,3 +421,18 @@ def test_near_pair_exact_s_factors(ser, r_over_h):
     for k in range(3):
         assert rel(ud[k].cpu().numpy(), udr[k]) <= 2e-15
         assert rel(vd[k].cpu().numpy(), vdr[k]) <= 2e-15
+
+
+def test_randomized_parity_sweep(ser, tmp_path):
+    """40 seeded random cases (tools/parity_sweep.py: sphere or ellipsoid with a random centre and
+    semi-axes, 1/h in {8, 12, 16, 24}, a random increasing rho in [1.5, 6], SL / DL / both,
+    polynomial or trigonometric densities, node + shell + far targets; every 5th case also the
+    s# variant) all within the 1e-12 bar of the oracle's localized mode."""
+    import importlib.util
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "parity_sweep.py")
+    spec = importlib.util.spec_from_file_location("parity_sweep", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.main(str(tmp_path / "sweep.json"), 40) == 0
