@@ -116,8 +116,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 //   v = 1/(2.5 + t) (tools/gen_sfactor_coeffs.py; |error of E| <= 2.1e-16 on [0.5, 6]);
 //   s2 = E - (2/sqrt pi) t e^{-t^2},  c23 = s2 - s3 = (2/sqrt pi)(2/3) t^3 e^{-t^2}.
 // Branch-free, no tables; for t < 0.5 it returns finite values the caller discards.
-__device__ __forceinline__ void sfactor_table(double t, const double* __restrict__ /*unused*/, double& E, double& s2,
-                                              double& c23, double* e_out = nullptr) {
+__device__ __forceinline__ void sfactor_s(double t, double& E, double& s2, double& c23, double* e_out = nullptr) {
   const double u = t * t;
   const double e = exp_neg(u);
   if (e_out) *e_out = e;  // e^{-t^2}, for callers that need it too (the s# factors)
@@ -153,10 +152,10 @@ __device__ __forceinline__ void sfactor_series_add(double t, double invd, double
 
 // NEXT-1 on-surface factors at one delta, t = r/delta:
 //   t >= 0.5: s1# = E + (2/(3 sqrt pi))(5t - 2t^3) e, s2# = E - (2/(3 sqrt pi))(3t - 14t^3 + 4t^5) e,
-//             s3# = E - (2/(9 sqrt pi))(9t + 6t^3 - 4t^5) e   (E, e from the same table/exp path)
+//             s3# = E - (2/(9 sqrt pi))(9t + 6t^3 - 4t^5) e   (E, e from the same exp + erfcx chain)
 //   t <  0.5: s#/t, s#/t^3, s#/t^5 from their series (coefficients generated and self-checked).
 // Returns A1 = s1#/r, A3 = s2#/r^3, A5 = s3#/r^5.
-__device__ __forceinline__ void sharp_weights(double r, double ri, double invd, const double* __restrict__ tab,
+__device__ __forceinline__ void sharp_weights(double r, double ri, double invd,
                                               double& A1, double& A3, double& A5) {
   const double t = r * invd;
   if (t < 0.5) {
@@ -175,7 +174,7 @@ __device__ __forceinline__ void sharp_weights(double r, double ri, double invd, 
     return;
   }
   double E, s2, c23, et;
-  sfactor_table(t, tab, E, s2, c23, &et);
+  sfactor_s(t, E, s2, c23, &et);
   const double e = et * kInvSqrtPi;  // e^{-t^2}/sqrt(pi), shared with E's evaluation
   const double t2 = t * t, t3 = t2 * t, t5 = t3 * t2;
   const double s1s = fma((2.0 / 3.0) * e, fma(-2.0, t3, 5.0 * t), E);

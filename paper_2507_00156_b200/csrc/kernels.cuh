@@ -578,14 +578,14 @@ struct NearAcc {
 template <int MODE, bool SHARP>
 __device__ __forceinline__ void near_pair(const Src& s, double y0, double y1, double y2,
                                           const double (*__restrict__ tf)[32], int lane, const NearParams& p,
-                                          const double* __restrict__ tab, NearAcc& a) {
+                                          NearAcc& a) {
   const double dx = y0 - s.x, dy = y1 - s.y, dz = y2 - s.z;
   const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
   const double ri = r2 > 0.0 ? rsqrt_nr(r2) : 0.0;
   const double r = r2 * ri;  // 0 for a coincident node
   if (SHARP) {  // NEXT-1: one delta, s# factors, unsplit stresslet (R16)
     double A1, A3, A5;
-    sharp_weights(r, ri, p.inv_delta[0], tab, A1, A3, A5);
+    sharp_weights(r, ri, p.inv_delta[0], A1, A3, A5);
     if (MODE & 1) {
       const double alpha = tf[NF_ALPHA][lane];
       const double gx = fma(-alpha, s.mx, s.fx), gy = fma(-alpha, s.my, s.fy), gz = fma(-alpha, s.mz, s.fz);
@@ -606,9 +606,9 @@ __device__ __forceinline__ void near_pair(const Src& s, double y0, double y1, do
   // all three deltas through the branch-free table path (independent chains)
   const double t0 = r * p.inv_delta[0], t1 = r * p.inv_delta[1], t2 = r * p.inv_delta[2];
   double E0, E1, E2, s20, s21, s22, c0, c1, c2;
-  sfactor_table(t0, tab, E0, s20, c0);
-  sfactor_table(t1, tab, E1, s21, c1);
-  sfactor_table(t2, tab, E2, s22, c2);
+  sfactor_s(t0, E0, s20, c0);
+  sfactor_s(t1, E1, s21, c1);
+  sfactor_s(t2, E2, s22, c2);
   const double tw0 = tf[NF_W0][lane], tw1 = tf[NF_W1][lane], tw2 = tf[NF_W2][lane];
   const double w0 = t0 >= 0.5 ? tw0 : 0.0, w1 = t1 >= 0.5 ? tw1 : 0.0, w2 = t2 >= 0.5 ? tw2 : 0.0;
   const double S1 = fma(w0, E0, fma(w1, E1, w2 * E2));
@@ -789,7 +789,7 @@ __device__ __forceinline__ void near_unit(const NearParams& p, int unit, NearSme
         const int sidx = q[head & (kQCap - 1)][lane];
         ++head;
         const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
-        near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, nullptr, acc);
+        near_pair<MODE, SHARP>(s, y0, y1, y2, tf, lane, p, acc);
       }
     }
     if (last) break;
