@@ -20,6 +20,28 @@ def shard_bounds(M: int, rank: int, world: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < rem else 0)
 
 
+def morton_order(tgt_xyz):
+    """Permutation sorting the targets by a 30-bit Morton key of their box-normalised
+    coordinates (10 bits per axis), so contiguous ranges of it are spatially compact
+    (contiguous ranges of Morton-sorted targets).  Index bookkeeping
+    only; ties keep input order (stable sort)."""
+    import torch
+
+    x = tgt_xyz
+    lo = x.min(dim=1, keepdim=True).values
+    ext = (x.max(dim=1, keepdim=True).values - lo).clamp_min(1e-300)
+    q = ((x - lo) / ext * 1023.0).clamp(0, 1023).to(torch.int64)
+
+    def spread(v):  # 10 bits -> every third bit
+        v = (v | (v << 16)) & 0x030000FF
+        v = (v | (v << 8)) & 0x0300F00F
+        v = (v | (v << 4)) & 0x030C30C3
+        return (v | (v << 2)) & 0x09249249
+
+    key = spread(q[0]) | (spread(q[1]) << 1) | (spread(q[2]) << 2)
+    return torch.sort(key, stable=True).indices
+
+
 def slice_targets(tgt_xyz, tgt_b, tgt_x0_density, start: int, stop: int):
     """Contiguous copies of one target range (SoA rows keep their layout)."""
     return (tgt_xyz[:, start:stop].contiguous(), tgt_b[start:stop].contiguous(),
@@ -54,11 +76,17 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
 
 
 def evaluate_sharded(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho, mode=3,
-                     group=None, gather: bool = True, evaluate_fn: Optional[Callable] = None):
+                     group=None, gather: bool = True, evaluate_fn: Optional[Callable] = None,
+                     morton: bool = True):
     """Evaluate this rank's target range against all sources; optionally all-gather.
 
+    With `morton` the ranges are contiguous in Morton order of the targets (each rank gets
+    a spatially compact set, so its 32-target warps keep tight boxes); the gathered result
+    is returned in the caller's order.  Without `gather`, a rank returns its own columns
+    (in Morton order when `morton`; `morton_order` gives the permutation).
     `evaluate_fn` defaults to the CUDA path (paper_2507_00156_b200.evaluate); it
     receives the same arguments with the local target arrays."""
+    import torch
     import torch.distributed as dist
 
     if evaluate_fn is None:
@@ -67,8 +95,25 @@ def evaluate_sharded(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     M = int(tgt_b.shape[0])
     a, b = shard_bounds(M, rank, world)
-    ty, tb, tx = slice_targets(tgt_xyz, tgt_b, tgt_x0_density, a, b)
+    if morton and world > 1:
+        perm = morton_order(tgt_xyz)
+        idx = perm[a:b]
+        ty, tb, tx = (tgt_xyz[:, idx].contiguous(), tgt_b[idx].contiguous(), tgt_x0_density[:, idx].contiguous())
+    else:
+        perm = None
+        ty, tb, tx = slice_targets(tgt_xyz, tgt_b, tgt_x0_density, a, b)
     u, v = evaluate_fn(src_xyz, src_normal, src_weight, f, q, ty, tb, tx, h, rho, mode=mode)
     if not gather or world == 1:
         return u, v
-    return (None if u is None else gather_columns(u, M, group)), (None if v is None else gather_columns(v, M, group))
+
+    def full(local):
+        if local is None:
+            return None
+        g = gather_columns(local, M, group)
+        if perm is None:
+            return g
+        out = torch.empty_like(g)
+        out[:, perm.to(g.device)] = g
+        return out
+
+    return full(u), full(v)

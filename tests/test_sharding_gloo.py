@@ -76,3 +76,19 @@ def test_gloo_world2_shard_and_gather(tmp_path):
     np.testing.assert_array_equal(np.load(tmp_path / "u.npy"), u_ref)
     np.testing.assert_array_equal(np.load(tmp_path / "v.npy"), v_ref)
     assert float(np.load(tmp_path / "t.npy")[0]) == 2.0  # max over ranks
+
+
+def test_morton_order_is_a_local_permutation():
+    """ranks take contiguous ranges of Morton-sorted targets.  The order is a
+    permutation, and consecutive targets in it are far closer than in a random order."""
+    import torch
+
+    from paper_2507_00156_b200.sharding import morton_order
+    from workloads.configs import config2
+
+    blk = config2(inv_h=16)
+    x = torch.from_numpy(blk.tgt_xyz)
+    p = morton_order(x)
+    assert sorted(p.tolist()) == list(range(blk.M))
+    step = lambda perm: float((x[:, perm[1:]] - x[:, perm[:-1]]).norm(dim=0).mean())
+    assert step(p) < 0.25 * step(torch.arange(blk.M))  # config 2 lists nodes, then a random shell
