@@ -6,7 +6,9 @@ h in {1/8, 1/12, 1/16, 1/24}, a strictly increasing rho triple in [1.5, 6], a mo
 densities (polynomial or trigonometric) and a target mix (nodes with b = 0, a shell with
 b ~ U[-4h, 4h], a few far targets), then compares stokes_er_eval with the oracle's localized
 mode (max-norm relative, u and v separately; the bar is 1e-12).  Every fifth case also runs
-the on-surface s# variant (random delta in [2h, 4h], cutoff 7) on the node targets.
+the on-surface s# variant (random delta in [2h, 4h], cutoff 7) on the node targets, and every
+fourth the treecode (random N0 in [40, 600), p in [2, 8], theta in [0.3, 0.8]) against the
+treecode oracle.
 
     python tools/parity_sweep.py OUT.json [n_cases]
 """
@@ -86,11 +88,22 @@ def main(out, n_cases=60):
                 row["sharp_rel_u"] = rel(us.cpu().numpy(), usr)
             if mode & 2:
                 row["sharp_rel_v"] = rel(vs.cpu().numpy(), vsr)
+        if seed % 4 == 1:  # NEXT-3: random treecode parameters against the treecode oracle
+            trng = np.random.default_rng(50_000 + seed)
+            n0, deg, th = int(trng.integers(40, 600)), int(trng.integers(2, 9)), float(trng.uniform(0.3, 0.8))
+            ut, vt = ser.evaluate_tree_block(blk, mode=mode, leaf_size=n0, degree=deg, theta=th)
+            utr, vtr = oracle.evaluate_tree_block(blk, mode=mode, leaf_size=n0, degree=deg, theta=th)
+            row["tree"] = [n0, deg, th]
+            if mode & 1:
+                row["tree_rel_u"] = rel(ut.cpu().numpy(), utr)
+            if mode & 2:
+                row["tree_rel_v"] = rel(vt.cpu().numpy(), vtr)
         rows.append(row)
         print(row, flush=True)
-    worst = max(v for r in rows for k, v in r.items() if k.startswith(("rel_", "sharp_rel_")))
-    res = {"what": "randomized parity sweep: stokes_er_eval (and every 5th case stokes_er_eval_onsurface) vs the "
-                   "oracle's localized mode, max-norm relative per output",
+    worst = max(v for r in rows for k, v in r.items() if k.startswith(("rel_", "sharp_rel_", "tree_rel_")))
+    res = {"what": "randomized parity sweep: stokes_er_eval (every 5th case also stokes_er_eval_onsurface, every "
+                   "4th also stokes_er_eval_tree with random N0, p, theta) vs the oracle's localized mode "
+                   "(treecode: vs the treecode oracle), max-norm relative per output",
            "cases": len(rows), "worst_rel": worst, "bar": 1e-12, "pass": bool(worst <= 1e-12),
            "seconds": time.time() - t0, "rows": rows}
     json.dump(res, open(out, "w"), indent=1)
