@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based); default configs[1]")
     ap.add_argument("--inv-h", type=int, default=64)
+    ap.add_argument("--eps", type=float, default=0.05, help="config 4: centre separation 2 + eps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
@@ -89,7 +90,7 @@ def make_workload(cfg: int, inv_h: int, rank: int):
         return config3(inv_h=inv_h, seed=seed)
     if cfg == 5:
         return config5(inv_h=inv_h, seed=seed)
-    raise SystemExit("bench configs: 1, 2, 3, 5, 6 = pure far (config 4 is a 4-block parity case)")
+    raise SystemExit("bench configs: 1, 2, 3, 5, 6 = pure far (config 4 has its own path: 4 blocks per step)")
 
 
 def near_pair_count(block) -> int:
@@ -406,6 +407,87 @@ def run_onsurface(args, rank, world):
     return line
 
 
+def run_config4(args, rank, world):
+    """BASELINE.json config 4: two unit spheres at centre separation 2 + eps (--eps), 1/h = --inv-h;
+    one step = the 4 block evaluations of the two-sphere field (A<-A, A<-B, B<-A, B<-B, each a
+    stokes_er_eval with targets = the nodes of one sphere); value = sum of the blocks' M N per second."""
+    import torch
+    from scipy.spatial import cKDTree
+
+    import paper_2507_00156_b200 as ser
+    from workloads.configs import config4
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    blocks = config4(eps=args.eps, inv_h=args.inv_h, seed=4 + 1000 * rank)
+    dblocks = [ser.to_device(b, dev) for b in blocks]
+    outs = [(torch.empty((3, b.M), dtype=torch.float64, device=dev), torch.empty((3, b.M), dtype=torch.float64,
+                                                                                  device=dev)) for b in blocks]
+    wss = [ser.alloc_workspace(b.M, b.N, 3, dev) for b in blocks]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        for b, arrs, (u, v), ws in zip(blocks, dblocks, outs, wss):
+            ser.evaluate(*arrs, b.h, b.rho, out_u=u, out_v=v, workspace=ws)
+
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(K):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            step()
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    from paper_2507_00156_b200.sharding import max_over_ranks
+    total_s = max_over_ranks(sum(ms) / 1e3, dev)
+    if rank != 0:
+        return None
+    pairs = sum(b.M * b.N for b in blocks)
+    near = sum(int(cKDTree(b.tgt_xyz.T).count_neighbors(cKDTree(b.src_xyz.T), 6.0 * max(b.rho) * b.h))
+               for b in blocks)
+    flops = (pairs - near) * F_FAR_ALG + near * F_NEAR_ALG
+    peak = SMS * FP64_LANES_PER_SM * 2 * 1965.0 * 1e6 / 1e12
+    achieved = flops / (total_s / K) / 1e12
+    line = {"metric": METRIC, "value": world * pairs * K / total_s, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg4_two_spheres_eps{args.eps}_h1/{args.inv_h}", "N_per_sphere": blocks[0].N,
+                       "blocks": [b.name for b in blocks], "pairs_per_step": pairs, "near_pairs_per_step": near,
+                       "rho": list(blocks[0].rho), "l2": "flushed between timed steps (256 MiB write)",
+                       "inputs": "resident in HBM"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": f"the 4 evaluations: {F_FAR_ALG} flops per far pair, {F_NEAR_ALG} per near pair",
+                         "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz"},
+            "clocks": clk.summary(), "gpu_launches": K * 4 * 7,
+            "gpu_launches_note": "per block: bbox, 2 morton, pack sources, pack targets, fused far+near, finalize "
+                                 "(+ CUB sort)",
+            "e2e": None}
+    if not args.no_cpu_baseline:
+        import oracle
+        rng = np.random.default_rng(0)
+        t_cpu, p_cpu = 0.0, 0
+        for b in blocks:  # ~2.5 s of oracle work per block
+            k = max(32, min(b.M, int(5e8 / b.N)))
+            sub = b.take_targets(np.sort(rng.choice(b.M, k, replace=False)))
+            t0 = time.perf_counter()
+            oracle.evaluate_block(sub, localized=True)
+            t_cpu += time.perf_counter() - t0
+            p_cpu += k * b.N
+        line["cpu_baseline"] = {"value": p_cpu / t_cpu, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                                "sample": f"random target samples of each of the 4 blocks, localized mode, "
+                                          f"{t_cpu:.1f} s wall"}
+    return line
+
+
 # PAPER.md Table 1 (lines 266-272): the paper's direct SL timing on 4 threads (MacBook Pro i7, 2.3 GHz)
 PAPER_TABLE1_4THREADS_S = {32: 1.0, 64: 11.0, 128: 155.0, 256: 2461.0}
 
@@ -605,6 +687,12 @@ def main():
 
     if args.workload == "tree" and args.impl == "ours":
         line = run_tree(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    if args.workload == "eval" and args.config == 4 and args.impl == "ours":
+        line = run_config4(args, rank, world)
         if line is not None:
             print(json.dumps(line), flush=True)
         return
