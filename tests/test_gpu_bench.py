@@ -32,3 +32,16 @@ def test_bench_json_line():
     e2e = d["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [["--config", "4", "--inv-h", "16", "--eps", "0.05"],
+                                  ["--workload", "onsurface", "--inv-h", "16"],
+                                  ["--workload", "tree", "--config", "5", "--inv-h", "32", "--tree", "500,4,0.6"]])
+def test_bench_other_workloads(args):
+    """The secondary bench workloads run and print one line with a positive value and a roofline."""
+    r = subprocess.run([sys.executable, "bench.py", *args, "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(s) for s in r.stdout.splitlines() if s.startswith("{")]
+    assert len(lines) == 1 and lines[0]["value"] > 0 and 0 < lines[0]["roofline"]["frac"] < 1
