@@ -1,19 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the B200 hot path (BASELINE.json metric).
 
-One step = one stokes_er_eval (SL+DL, 3-delta localized regularization with the
-fused extrapolation) over BASELINE.json configs[1] at 1/h = 64: the unit
-sphere's N = 68,166 quadrature nodes as sources, M = 102,249 targets (all nodes
-at b = 0 plus N/2 shell targets, b ~ U[-3h, 3h]), rho = (2,3,4), seeded cubic
-densities.  Inputs are resident in HBM when the timed region starts; L2 is
-flushed (256 MiB write) between timed steps.
+One step = one full SL+DL evaluation (3-delta localized regularization with the
+fused extrapolation, stokes_er_eval) of BASELINE.json configs[4] at 1/h = 256:
+the unit sphere's N = 1,090,854 quadrature nodes as sources and every node a
+target (M = N, b = 0), rho = (2,3,4), seeded cubic densities -- the largest
+single-GPU configuration, at N >= 1e5 where north_star states its bar.  Inputs
+are resident in HBM when the timed region starts; L2 is flushed (256 MiB write)
+between timed steps.  Other configs: --config 1..6 --inv-h H (6 = pure far).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  Multi-GPU (torchrun): targets are independent
-(PAPER.md:167-169), so every rank evaluates its own seeded instance of the
-workload with no data-path collective ("weak" scaling); value = all ranks'
-pairs / max-over-ranks device time.
+Prints ONE JSON line (rank 0).  Multi-GPU (torchrun, NCCL): ONE seeded target
+set is split across the ranks (sharding.evaluate_sharded: contiguous ranges of
+the Morton-sorted targets, sources replicated, one all-gather of u, v inside
+the timed region) -- strong scaling, value =
+the block's pairs / max-over-ranks device time.
 """
 from __future__ import annotations
 
@@ -51,24 +53,23 @@ FP64_LANES_PER_SM = 64  # measured: DFMA loop 58.7 FMA/clk/SM at the boost clock
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config index (1-based); default configs[1]")
-    ap.add_argument("--inv-h", type=int, default=64)
+    ap.add_argument("--config", type=int, default=5, help="BASELINE.json config index (1-based); default configs[4] (the N >= 1e5 sweep the north_star bar is stated at; 6 = pure-far micro-config)")
+    ap.add_argument("--inv-h", type=int, default=256)
     ap.add_argument("--eps", type=float, default=0.05, help="config 4: centre separation 2 + eps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--targets-per-thread", type=int, default=0)
     ap.add_argument("--near-phases", type=int, default=0)
     ap.add_argument("--chunk-tiles", type=int, default=0, help="far item = chunk x 128 sources (0: automatic)")
-    ap.add_argument("--workload", choices=["eval", "twodrop", "tree", "spheroid", "onsurface"], default="eval",
+    ap.add_argument("--workload", choices=["eval", "twodrop", "tree", "onsurface"], default="eval",
                     help="eval: one stokes_er_eval of BASELINE.json config --config (default); "
                          "onsurface: one stokes_er_eval_onsurface (NEXT-1, s#, delta = 3h) of config 5 "
                          "(every node a target) at 1/h = --inv-h; "
                          "twodrop: one GMRES solve of the NEXT-2 two-drop IE (35) at 1/h = --inv-h; "
-                         "tree: one stokes_er_eval_tree (NEXT-3) of config --config at 1/h = --inv-h; "
-                         "spheroid: PAPER.md Table 1's SL evaluation at 1/h = --inv-h")
+                         "tree: one stokes_er_eval_tree (NEXT-3) of config --config at 1/h = --inv-h")
     ap.add_argument("--tree", type=str, default="",
                     help="treecode N0,p,theta (default: PAPER.md eq. (33) policy for --inv-h)")
     ap.add_argument("--schedule", choices=["fused", "separate"], default="fused",
@@ -97,7 +98,8 @@ def near_pair_count(block) -> int:
     """Pairs with r <= 6 delta_max (the near rule of include/stokes_er.h), by KD-tree."""
     from scipy.spatial import cKDTree
     rc = 6.0 * max(block.rho) * block.h
-    return int(cKDTree(block.tgt_xyz.T).count_neighbors(cKDTree(block.src_xyz.T), rc))
+    counts = cKDTree(block.src_xyz.T).query_ball_point(block.tgt_xyz.T, rc, return_length=True, workers=-1)
+    return int(np.asarray(counts, dtype=np.int64).sum())
 
 
 class ClockSampler:
@@ -115,13 +117,25 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0:  # sampler running before the timed region
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
+
+    def pad(self, busy, min_samples=5, limit_s=5.0):
+        """Short timed regions see few 50 ms samples: keep the GPU busy with untimed steps
+        (`busy()`) until the record holds `min_samples` (clocks under the same load)."""
+        if self.proc is None:
+            return
+        t0 = time.time()
+        while len(self.lines) < min_samples and time.time() - t0 < limit_s:
+            busy()
 
     def _read(self):
         for line in self.proc.stdout:
@@ -193,41 +207,6 @@ def run_reference(args, rank, world):
             "cpu_baseline": cpu, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                                          "d2h_bytes_per_step": 0}}
 
-
-def cpu_baseline(block):
-    """The oracle (localized) on the host cores, bounded sample of ~10 s of CPU work."""
-    import oracle
-    cores = oracle.max_threads()
-    rng = np.random.default_rng(1)
-    k = 256
-    t0 = time.perf_counter()
-    oracle.evaluate_block(block.take_targets(rng.choice(block.M, k, replace=False)), localized=True)
-    per_target = (time.perf_counter() - t0) / k
-    k = int(min(block.M, max(256, 10.0 / per_target)))
-    idx = rng.choice(block.M, k, replace=False)
-    t0 = time.perf_counter()
-    oracle.evaluate_block(block.take_targets(idx), localized=True)
-    dt = time.perf_counter() - t0
-    return {"value": k * block.N / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{k} random targets of {block.M} x all {block.N} sources, localized mode "
-                      f"(paper's shared-far-field algorithm), {dt:.1f} s wall"}
-
-
-def committed_traffic(fused: bool):
-    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
-    `ncu --set full` summary of this bench command (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_v16_fused.json")
-    if not fused or not os.path.exists(path):
-        return None
-    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for k in json.load(open(path))["kernels"]:
-        if k["kernel"].startswith("void fused_kernel<3, 2"):
-            tot = 0.0
-            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                v, u = k[key].split()
-                tot += float(v) * units[u]
-            return int(tot), "profiles/r01/ncu_full_v16_fused.json (one ncu --set full capture of this command)"
-    return None
 
 def twodrop_launches(it: int) -> int:
     """Our kernel launches in one stokes_er_twodrop_solve that took `it` Krylov steps."""
@@ -488,67 +467,6 @@ def run_config4(args, rank, world):
     return line
 
 
-# PAPER.md Table 1 (lines 266-272): the paper's direct SL timing on 4 threads (MacBook Pro i7, 2.3 GHz)
-PAPER_TABLE1_4THREADS_S = {32: 1.0, 64: 11.0, 128: 155.0, 256: 2461.0}
-
-
-def run_spheroid(args, rank, world):
-    """PAPER.md Sec. 4.1 / Table 1: one SL evaluation (3-delta extrapolation, rho = (3,4,5),
-    localized) of the Stokeslet integral at the grid points within h outside the translating
-    prolate spheroid; value = pair interactions/s (M N / time); vs_baseline against the
-    paper's own 4-thread time for the same workload; errors vs the exact velocity."""
-    import torch
-
-    import paper_2507_00156_b200 as ser
-    from workloads.spheroid import spheroid_block
-
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev = torch.device(f"cuda:{local}")
-    torch.cuda.set_device(dev)
-    blk = spheroid_block(args.inv_h)
-    M, N = blk.M, blk.N
-    arrs = ser.to_device(blk, dev)
-    u = torch.empty((3, M), dtype=torch.float64, device=dev)
-    ws = ser.alloc_workspace(M, N, 1, dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    K, W = args.steps, args.warmup
-    for _ in range(W):
-        flush.zero_()
-        ser.evaluate(*arrs, blk.h, blk.rho, mode=1, out_u=u, workspace=ws)
-    torch.cuda.synchronize(dev)
-    ms = []
-    with ClockSampler(local) as clk:
-        for _ in range(K):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            ser.evaluate(*arrs, blk.h, blk.rho, mode=1, out_u=u, workspace=ws)
-            b.record()
-            b.synchronize()
-            ms.append(a.elapsed_time(b))
-    from paper_2507_00156_b200.sharding import max_over_ranks
-    total_s = max_over_ranks(sum(ms) / 1e3, dev)
-    if rank != 0:
-        return None
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from closed_forms import spheroid_translation_velocity
-    err = np.linalg.norm(u.cpu().numpy() - spheroid_translation_velocity(blk.tgt_xyz), axis=0)
-    value = world * M * N * K / total_s
-    paper_s = PAPER_TABLE1_4THREADS_S.get(args.inv_h)
-    line = {"metric": "Stokeslet (SL) 3-delta extrapolated evaluation on the translating spheroid (PAPER.md Table 1): "
-                      "pair interactions/sec", "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-            "warmup": W, "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": (value / (M * N / paper_s)) if paper_s else None,
-            "vs_baseline_note": (f"paper's direct sum, 4 threads, {paper_s} s (PAPER.md Table 1, MacBook Pro "
-                                 "2.3 GHz i7): another machine, context") if paper_s else None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": blk.name, "N": N, "M": M, "rho": list(blk.rho), "mode": "SL",
-                       "max_err": float(err.max()), "l2_err": float(np.sqrt((err ** 2).mean())),
-                       "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM"},
-            "clocks": clk.summary(), "gpu_launches": K * ser.launch_count(M, N, 1), "e2e": None}
-    return line
-
-
 def run_twodrop(args, rank, world):
     """NEXT-2 bench: one step = one full GMRES solve of IE (35) (Sec. 4.3)
     on the two drops at 1/h = args.inv_h through stokes_er_twodrop_solve: 4 block
@@ -673,51 +591,139 @@ def run_twodrop(args, rank, world):
     return line
 
 
-def main():
-    args = parse()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+def committed_traffic(bench_cfg: dict, kernel_prefix: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from a committed
+    `ncu --set full` summary (profiles/*/ncu_full_*.json) whose recorded bench
+    configuration equals this run's (workload, path, schedule, targets per thread);
+    None when no capture of this exact command exists."""
+    import glob
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    keys = ("workload", "path", "schedule", "targets_per_thread")
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_full_*.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except (OSError, ValueError):
+            continue
+        meta = d.get("bench_config")
+        if not meta or any(meta.get(k) != bench_cfg.get(k) for k in keys):
+            continue
+        for k in d.get("kernels", []):
+            if k["kernel"].startswith(kernel_prefix) and "dram__bytes_read.sum" in k:
+                tot = 0.0
+                for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, u = k[key].split()
+                    tot += float(v.replace(",", "")) * units[u]
+                return int(tot), os.path.relpath(path, ROOT) + " (ncu --set full capture of this bench configuration)"
+    return None
 
-    if args.workload == "spheroid" and args.impl == "ours":
-        line = run_spheroid(args, rank, world)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        return
 
-    if args.workload == "tree" and args.impl == "ours":
-        line = run_tree(args, rank, world)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        return
+def sampled_parity(block, u_gpu, v_gpu, n=48, seed=7):
+    """Max-norm relative error of the GPU output against the oracle's DEFINITION mode
+    (every pair regularized for every delta: the parity reference) on a seeded sample
+    of n targets x all N sources.  Returns (record, oracle seconds, pairs)."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(block.M, min(n, block.M), replace=False))
+    sub = block.take_targets(idx)
+    t0 = time.perf_counter()
+    ur, vr = oracle.evaluate_block(sub, localized=False)
+    dt = time.perf_counter() - t0
+    eu = float(np.abs(u_gpu[:, idx] - ur).max() / np.abs(ur).max())
+    ev = float(np.abs(v_gpu[:, idx] - vr).max() / np.abs(vr).max())
+    return {"u_max_rel": eu, "v_max_rel": ev, "targets_sampled": int(len(idx)), "sample_seed": seed,
+            "reference": "oracle definition mode (every pair, every delta), same seeded inputs",
+            "tolerance": 1e-12}, dt, len(idx) * block.N
 
-    if args.workload == "eval" and args.config == 4 and args.impl == "ours":
-        line = run_config4(args, rank, world)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        return
 
-    if args.workload == "onsurface" and args.impl == "ours":
-        line = run_onsurface(args, rank, world)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        return
+def solve_parity(block, dev, stream):
+    """The 3x3 extrapolation solve alone (stokes_er_extrapolate vs the oracle's pivoted
+    elimination) on seeded per-delta values: the workload's own b values (a sample) and
+    b spread over [-6 delta_3, 6 delta_3]; tolerance 1e-13 (north_star)."""
+    import torch
 
-    if args.workload == "twodrop" and args.impl == "ours":
-        line = run_twodrop(args, rank, world)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        return
+    import oracle
+    import paper_2507_00156_b200 as ser
+    rng = np.random.default_rng(11)
+    b = np.concatenate([rng.choice(block.tgt_b, 128),
+                        rng.uniform(-6, 6, 128) * max(block.rho) * block.h, [0.0]])
+    ind = rng.uniform(-1, 1, (3, 6, b.size))
+    got = ser.extrapolate(torch.from_numpy(b).to(dev), block.h, block.rho, torch.from_numpy(ind).to(dev),
+                          stream=stream).cpu().numpy()
+    ref = oracle.extrapolate(b, block.h, block.rho, ind)
+    return float(np.abs(got - ref).max() / np.abs(ref).max())
 
-    if args.impl == "reference":
-        line = run_reference(args, rank, world)
-        if line is not None:
-            print(json.dumps(line), flush=True)
-        return
+
+def cpu_baseline(block, definition=None):
+    """The oracle on the host cores, as it stands, on bounded target samples:
+    localized mode (the paper's shared-far-field algorithm) on all cores is
+    `value`; definition mode (every pair regularized: the parity reference) and one-core
+    timings of both modes sit beside it.  ~20 s of CPU work in total."""
+    import oracle
+    cores = oracle.max_threads()
+    rng = np.random.default_rng(1)
+
+    def rate(localized, nthreads, budget_s):
+        k = 8
+        t0 = time.perf_counter()
+        oracle.evaluate_block(block.take_targets(rng.choice(block.M, k, replace=False)), localized=localized,
+                              nthreads=nthreads)
+        per_target = (time.perf_counter() - t0) / k
+        k = int(min(block.M, max(8, budget_s / per_target)))
+        idx = rng.choice(block.M, k, replace=False)
+        t0 = time.perf_counter()
+        oracle.evaluate_block(block.take_targets(idx), localized=localized, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        return k * block.N / dt, k, dt
+
+    v, k, dt = rate(True, 0, 10.0)
+    rec = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{k} random targets of {block.M} x all {block.N} sources, localized mode "
+                     f"(the paper's shared-far-field algorithm, P:183-191), {dt:.1f} s wall on {cores} threads"}
+    if definition is not None:
+        dsec, dpairs = definition
+        rec["definition_mode"] = {"value": dpairs / dsec, "unit": UNIT, "cores": cores,
+                                  "sample": f"the parity sample ({dpairs // block.N} targets x all sources), "
+                                            f"{dsec:.1f} s wall"}
+    v1, k1, dt1 = rate(True, 1, 4.0)
+    rec["one_core_localized"] = {"value": v1, "unit": UNIT, "cores": 1,
+                                 "sample": f"{k1} targets x all sources, {dt1:.1f} s wall"}
+    v2, k2, dt2 = rate(False, 1, 4.0)
+    rec["one_core_definition"] = {"value": v2, "unit": UNIT, "cores": 1,
+                                  "sample": f"{k2} targets x all sources, {dt2:.1f} s wall"}
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except (OSError, IndexError):
+        model = None
+    rec["cpu_model"] = model
+    return rec
+
+
+def sharded_step(arrs, block, evaluate_fn):
+    """The multi-rank step of run_eval: this rank's Morton range of ONE target set against
+    all sources, then the all-gather of u, v back into the caller's order
+    (sharding.evaluate_sharded)."""
+    from paper_2507_00156_b200 import sharding
+    return sharding.evaluate_sharded(*arrs, block.h, block.rho, mode=3, gather=True, evaluate_fn=evaluate_fn)
+
+
+def run_eval(args, rank, world):
+    """The default bench: one step = one full SL+DL 3-delta evaluation (stokes_er_eval)
+    of BASELINE.json config --config at 1/h = --inv-h (default config 5 at 1/h = 256:
+    the unit sphere's N = M = 1,090,854 nodes, every node a target at b = 0).
+
+    N = 1: one process evaluates the whole block.  N > 1 (torchrun, NCCL): ONE seeded
+    target set split across the ranks by sharding.evaluate_sharded (contiguous ranges
+    of the Morton-sorted targets, sources replicated, the all-gather of u, v inside the
+    timed region) -- strong scaling, value = the
+    block's M N pairs / max-over-ranks time."""
+    import ctypes
 
     import torch
-    import paper_2507_00156_b200 as ser
 
+    import paper_2507_00156_b200 as ser
+    from paper_2507_00156_b200.sharding import max_over_ranks, shard_bounds
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -726,13 +732,12 @@ def main():
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
 
-    block = make_workload(args.config, args.inv_h, rank)
+    block = make_workload(args.config, args.inv_h, 0)  # one target set for every rank (strong scaling)
     M, N = block.M, block.N
     pairs = M * N
-    near = near_pair_count(block)
+    a0, a1 = shard_bounds(M, rank, world)
+    M_loc = a1 - a0
     arrs = ser.to_device(block, dev)
-    out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
-    out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
     opt = ser.Options()
     if args.targets_per_thread:
         opt.targets_per_thread = args.targets_per_thread
@@ -742,19 +747,28 @@ def main():
         opt.source_chunk_tiles = args.chunk_tiles
     fused = args.schedule != "separate"
     opt.schedule = {"fused": 0, "separate": 1}[args.schedule]
-    nbytes = int(ser._lib.load().stokes_er_workspace_bytes_ex(M, N, 3, __import__("ctypes").byref(opt)))
-    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    L = ser._lib.load()
+    ws = torch.empty(int(L.stokes_er_workspace_bytes_ex(M_loc, N, 3, ctypes.byref(opt))), dtype=torch.uint8,
+                     device=dev)
+    out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+    out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     K, W = args.steps, args.warmup
 
-    def step(ev_pair=None, ev_near=None):
+    def local_eval(sx, sn, sw, f, q, ty, tb, tx, h, rho, mode=3, ev_pair=None, ev_near=None, ou=None, ov=None):
         opt.pair_kernel_start_event = ev_pair[0].cuda_event if ev_pair else None
         opt.pair_kernel_end_event = ev_pair[1].cuda_event if ev_pair else None
         opt.near_kernel_start_event = ev_near[0].cuda_event if ev_near else None
         opt.near_kernel_end_event = ev_near[1].cuda_event if ev_near else None
-        ser.evaluate(*arrs, block.h, block.rho, out_u=out_u, out_v=out_v, workspace=ws, stream=stream,
-                     options=opt)
+        return ser.evaluate(sx, sn, sw, f, q, ty, tb, tx, h, rho, mode=mode, out_u=ou, out_v=ov, workspace=ws,
+                            stream=stream, options=opt)
+
+    def step(ev_pair=None, ev_near=None):
+        if world == 1:
+            local_eval(*arrs, block.h, block.rho, ev_pair=ev_pair, ev_near=ev_near, ou=out_u, ov=out_v)
+            return out_u, out_v
+        return sharded_step(arrs, block, lambda *a, **kw: local_eval(*a, ev_pair=ev_pair, ev_near=ev_near, **kw))
 
     for _ in range(W):
         flush.zero_()
@@ -767,35 +781,48 @@ def main():
     for a, b in evp + evn:  # torch creates the CUDA event lazily on first record: materialize the handles
         a.record(stream)
         b.record(stream)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
         for i in range(K):
             flush.zero_()  # L2 flush, outside the timed events
             ev[i][0].record(stream)
-            step(evp[i], evn[i])
+            res_u, res_v = step(evp[i], evn[i])
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clk.pad(lambda: (step(), torch.cuda.synchronize(dev)))
     step_ms = [a.elapsed_time(b) for a, b in ev]
     pair_ms = [a.elapsed_time(b) for a, b in evp]
     near_ms = [a.elapsed_time(b) for a, b in evn]
-    from paper_2507_00156_b200.sharding import max_over_ranks
     total_s = max_over_ranks(sum(step_ms) / 1e3, dev)
-    value = world * pairs * K / total_s
+    value = pairs * K / total_s
+    u_host, v_host = res_u.cpu().numpy(), res_v.cpu().numpy()
 
-    # end-to-end through the C ABI with pinned HOST buffers (copies inside the timed region)
+    # end to end through the public API with pinned HOST buffers (copies inside the timed region):
+    # N = 1: stokes_er_eval_host (H2D, evaluate, D2H in the library); N > 1: H2D of the inputs,
+    # evaluate_sharded (incl. the all-gather), D2H of the gathered u, v
     e2e = None
     if not args.no_e2e:
         host = [torch.from_numpy(a).pin_memory() for a in block.arrays()]
         hu = torch.empty((3, M), dtype=torch.float64).pin_memory()
         hv = torch.empty((3, M), dtype=torch.float64).pin_memory()
-        hws = ser.alloc_workspace(M, N, 3, dev, host=True)
+        if world == 1:
+            hws = ser.alloc_workspace(M, N, 3, dev, host=True)
+            e_step = lambda: ser.evaluate_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws,
+                                               stream=stream)
+        else:
+            def e_step():
+                d = [t.to(dev, non_blocking=True) for t in host]
+                uu, vv = sharded_step(d, block, local_eval)
+                hu.copy_(uu, non_blocking=True)
+                hv.copy_(vv, non_blocking=True)
         for _ in range(2):
-            ser.evaluate_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws, stream=stream)
+            e_step()
+        torch.cuda.synchronize(dev)
         ke = max(3, K // 4)
         if dist is not None:
             dist.barrier()
@@ -805,85 +832,125 @@ def main():
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            ser.evaluate_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws, stream=stream)
+            e_step()
             b.record(stream)
             b.synchronize()
             e_ms.append(a.elapsed_time(b))
         e_total = max_over_ranks(sum(e_ms) / 1e3, dev)
-        e2e = {"value": world * pairs * ke / e_total, "unit": UNIT,
+        e2e = {"value": pairs * ke / e_total, "unit": UNIT,
                "h2d_bytes_per_step": int(sum(a.nbytes for a in block.arrays())),
-               "d2h_bytes_per_step": int(hu.numel() * 8 + hv.numel() * 8)}
+               "d2h_bytes_per_step": int(hu.numel() * 8 + hv.numel() * 8),
+               "api": "stokes_er_eval_host (C ABI, pinned host buffers)" if world == 1 else
+                      "host->device copies + sharding.evaluate_sharded (all-gather) + device->host copy"}
 
+    sol_err = solve_parity(block, dev, stream) if rank == 0 else None
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
-        return
+        return None
 
+    near = near_pair_count(block)
     clocks = clk.summary()
     far_avg_s = statistics.mean(pair_ms) / 1e3
     far = pairs - near
+    # per-rank kernel work: the local target range's share (Morton ranges: near pairs ~ uniform)
+    share = M_loc / M
     f_clk = 1965.0
     peak = SMS * FP64_LANES_PER_SM * 2 * f_clk * 1e6 / 1e12  # TFLOP/s
-    peak_source = "derived: 148 SMs x 64 FP64 FMA/clk/SM (DFMA-loop probe) x 2 x 1965 MHz max SM clock"
+    peak_source = ("derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz max SM clock (MEASURED_PEAKS.json has "
+                   "no FP64 entry; DFMA-loop probe 34.2 TFLOP/s = 92% of it, tools/probes)")
     if fused:
-        # the dominant (and only pair) kernel does the far AND the near pairs
-        k_flops = far * F_FAR_ALG + near * F_NEAR_ALG
-        k_issued = far * F_FAR_ISSUED + near * F_NEAR_ISSUED
+        k_flops = (far * F_FAR_ALG + near * F_NEAR_ALG) * share
+        k_issued = (far * F_FAR_ISSUED + near * F_NEAR_ISSUED) * share
         kname = ("fused_kernel<3,T> (FP64 pipe): far-field sum (PAPER.md:183-191) + near 3-delta sums "
                  "with the folded extrapolation (PAPER.md:82-123), one persistent kernel")
+        kprefix = "void ser::fused_kernel<3"
         conv = (f"{F_FAR_ALG} algorithmic flops per far pair + {F_NEAR_ALG} per near pair "
                 "(rsqrt/erf/exp = 1, FMA = 2)")
     else:
-        k_flops = far * F_FAR_ALG
-        k_issued = far * F_FAR_ISSUED
+        k_flops = far * F_FAR_ALG * share
+        k_issued = far * F_FAR_ISSUED * share
         kname = "far_kernel<3,T> (FP64 pipe): the shared far-field sum, PAPER.md:183-191"
+        kprefix = "void ser::far_kernel<3"
         conv = f"{F_FAR_ALG} algorithmic flops per far pair (rsqrt = 1, FMA = 2)"
     achieved = k_flops / far_avg_s / 1e12
+    bench_cfg = {"workload": block.name, "path": "stokes_er_eval", "schedule": args.schedule,
+                 "targets_per_thread": int(opt.stats[3])}
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": kname, "peak_source": peak_source,
+                "traffic": None, "traffic_source": "no ncu --set full capture of this exact configuration committed",
+                "kernel": kname, "peak_source": peak_source,
                 "flops_per_launch": k_flops, "flop_convention": conv,
                 "frac_issued_convention": k_issued / far_avg_s / 1e12 / peak,
-                "kernel_ms": far_avg_s * 1e3,
-                "kernel_share": sum(pair_ms) / sum(step_ms),
+                "kernel_ms": far_avg_s * 1e3, "kernel_share": sum(pair_ms) / sum(step_ms),
+                "timing": "CUDA events recorded by the library around the kernel on the launching stream",
                 "far_pairs": far, "near_pairs": near}
-    traffic = committed_traffic(fused)
+    traffic = committed_traffic(bench_cfg, kprefix)
     if traffic:
         roofline["traffic"], roofline["traffic_source"] = traffic
     if clocks.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (SMS * FP64_LANES_PER_SM * 2 * clocks["sm_mhz"] / 1e6)
-    if fused:
-        near_info = None
-    else:
+    near_info = None
+    if not fused:
         near_avg_s = statistics.mean(near_ms) / 1e3
-        roofline["far_pairs_per_s"] = far / far_avg_s
+        roofline["far_pairs_per_s"] = far * share / far_avg_s
         near_info = {"kernel": "near_kernel<3>", "ms": near_avg_s * 1e3, "share": sum(near_ms) / sum(step_ms),
-                     "near_pairs": near, "near_pairs_per_s": near / near_avg_s,
-                     "tflops_alg": near * F_NEAR_ALG / near_avg_s / 1e12}
+                     "near_pairs": near, "near_pairs_per_s": near * share / near_avg_s,
+                     "tflops_alg": near * share * F_NEAR_ALG / near_avg_s / 1e12}
     alg_flops = far * F_FAR_ALG + near * F_NEAR_ALG
+    parity, def_s, def_pairs = sampled_parity(block, u_host, v_host)
+    parity["solve_max_rel"] = sol_err
+    parity["solve_tolerance"] = 1e-13
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": 1e3 * total_s / K, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": block.name, "N": N, "M": M, "pairs_per_step": pairs, "near_pairs_per_step": near,
                        "h": block.h, "rho": list(block.rho), "mode": "SL+DL", "cutoff": 6.0,
-                       "l2": "flushed between timed steps (256 MiB write)", "inputs": "resident in HBM",
+                       "l2": "flushed between timed steps (256 MiB write); inputs are larger than L2 at N >= 1e6",
+                       "inputs": "resident in HBM", "seed": block.meta.get("seed"),
                        "targets_per_thread": int(opt.stats[3]), "work_items": int(opt.stats[0]),
                        "grid_ctas": int(opt.stats[1]), "chunk_tiles": int(opt.stats[2]),
-                       "schedule": args.schedule,
-                       "parallelism": f"target-sharded x{world} (independent instances)"},
-            "fp64_tflops_alg": alg_flops * K * world / total_s / 1e12,
-            "roofline": roofline, "clocks": clocks,
-            "gpu_launches": K * (ser.launch_count(M, N, 3) + (0 if fused else 1)),
-            "gpu_launches_note": "our kernels per step: bbox, 2 morton, pack_sources, pack_targets, "
+                       "schedule": args.schedule, "path": "stokes_er_eval",
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"target-sharded x{world}: Morton ranges of ONE target set "
+                                       "(sharding.evaluate_sharded), sources replicated, all-gather of u, v in the "
+                                       "timed region")},
+            "fp64_tflops_alg": alg_flops * K / total_s / 1e12,
+            "roofline": roofline, "clocks": clocks, "parity": parity,
+            "gpu_launches": K * (ser.launch_count(M_loc, N, 3) + (0 if fused else 1)),
+            "gpu_launches_note": "our kernels per step and rank: bbox, 2 morton, pack_sources, pack_targets, "
                                  + ("fused far+near" if fused else "far, near") + ", finalize "
                                  "(+ CUB radix-sort launches, library code)",
             "e2e": e2e}
     if near_info is not None:
         line["near_kernel"] = near_info
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(block)
-    print(json.dumps(line), flush=True)
+        line["cpu_baseline"] = cpu_baseline(block, definition=(def_s, def_pairs))
     if dist is not None:
         dist.destroy_process_group()
+    return line
+
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    elif args.workload == "tree":
+        line = run_tree(args, rank, world)
+    elif args.workload == "onsurface":
+        line = run_onsurface(args, rank, world)
+    elif args.workload == "twodrop":
+        line = run_twodrop(args, rank, world)
+    elif args.config == 4:
+        line = run_config4(args, rank, world)
+    else:
+        line = run_eval(args, rank, world)
+    if line is not None:
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -291,7 +291,7 @@ int stokes_er_twodrop_solve(const stokes_er_drop drops[2], const stokes_er_cross
  * (gap > STOKES_ER_CUTOFF max delta_k, so no near pair is approximated), else
  * its children are checked; a leaf that fails is summed directly with the
  * localized 3-delta regularization.  The extrapolation is as in stokes_er_eval.
- * The paper's parameter policy (eq. (33), PAPER.md:316-318): theta = 0.6,
+ * The paper's parameter policy (eq. (33), PAPER.md:297-300): theta = 0.6,
  * N0 = 2000 and p = 6 at h = 1/64, N0 doubling and p + 2 per halving of h.
  *
  * Plan: HOST memory of stokes_er_tree_plan_bytes(N, params) bytes, written by

@@ -613,6 +613,9 @@ static int eval_tree_impl(const double* src_xyz, const double* src_normal, const
   const double delta[3] = {rho[0] * h, rho[1] * h, rho[2] * h};
   const double cutoff = sharp ? 7.0 : ORACLE_CUTOFF;  /* R15 for s# */
   const double rc2 = (cutoff * delta[2]) * (cutoff * delta[2]);
+  /* R23 guard margin: a cluster whose box gap is within rounding of the cutoff is
+   * never approximated, so no pair the near rule (r^2 <= rc2) owns can be */
+  const double rc2_guard = rc2 * (1.0 + 1e-9);
   const int nd = sharp ? 1 : 3;
   double* ud = (double*)malloc(sizeof(double) * 9 * (size_t)(M > 0 ? M : 1));
   double* vd = (double*)malloc(sizeof(double) * 9 * (size_t)(M > 0 ? M : 1));
@@ -652,7 +655,7 @@ static int eval_tree_impl(const double* src_xyz, const double* src_normal, const
         if (gap < 0.0) gap = 0.0;
         g2 = g2 + gap * gap;
       }
-      const int accept = (t->rc <= theta * sqrt(R2)) && (g2 > rc2);
+      const int accept = (t->rc <= theta * sqrt(R2)) && (g2 > rc2_guard);
       if (accept && t->end - t->begin > NP) { /* eq. (31): unregularized kernels at the Chebyshev points */
         n_acc += 1.0;
         const double* G = T.mw + (size_t)c * NP * TC_CH;

@@ -66,17 +66,30 @@ def alloc_workspace(M: int, N: int, mode: int = BOTH, device="cuda", host=False)
     return torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
 
 
-def _shapes(src_xyz, tgt_b):
-    return int(tgt_b.shape[0]), int(src_xyz.shape[1])
-
-
-def evaluate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho, mode=BOTH,
-             out_u=None, out_v=None, workspace=None, stream=None, options: "_lib.Options | None" = None):
-    """stokes_er_eval on device tensors; returns (u (3,M) or None, v (3,M) or None).
-    Asynchronous on `stream` (default: torch's current stream)."""
+def _scratch(nbytes, dev, stream):
+    """Temporary device buffer for one call, allocated on `dev` and tied to `stream`:
+    the caching allocator must not hand it out again while the call's kernels run
+    on a stream other than torch's current one."""
     torch = _torch()
+    with torch.cuda.device(dev):
+        t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
+    if stream is not None:
+        t.record_stream(stream)
+    return t
+
+
+def _out(shape, dev, stream):
+    torch = _torch()
+    with torch.cuda.device(dev):
+        t = torch.empty(shape, dtype=torch.float64, device=dev)
+    if stream is not None:
+        t.record_stream(stream)
+    return t
+
+
+def _check_inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, mode):
+    """Shapes/dtypes/devices of the hot-path inputs (raises before any launch)."""
     M, N = _shapes(src_xyz, tgt_b)
-    dev = src_xyz.device
     _check_dev("src_xyz", src_xyz, (3, N))
     _check_dev("src_normal", src_normal, (3, N))
     _check_dev("src_weight", src_weight, (N,))
@@ -85,17 +98,36 @@ def evaluate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_densi
     _check_dev("tgt_xyz", tgt_xyz, (3, M))
     _check_dev("tgt_b", tgt_b, (M,))
     _check_dev("tgt_x0_density", tgt_x0_density, (9, M))
+    dev = src_xyz.device
+    for name, t in (("src_normal", src_normal), ("src_weight", src_weight), ("f", f if mode & SL else None),
+                    ("q", q if mode & DL else None), ("tgt_xyz", tgt_xyz), ("tgt_b", tgt_b),
+                    ("tgt_x0_density", tgt_x0_density)):
+        if t is not None and t.device != dev:
+            raise ValueError(f"{name}: on {t.device}, expected {dev} (all inputs on one device)")
+    return M, N, dev
+
+
+def _shapes(src_xyz, tgt_b):
+    return int(tgt_b.shape[0]), int(src_xyz.shape[1])
+
+
+def evaluate(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho, mode=BOTH,
+             out_u=None, out_v=None, workspace=None, stream=None, options: "_lib.Options | None" = None):
+    """stokes_er_eval on device tensors; returns (u (3,M) or None, v (3,M) or None).
+    Asynchronous on `stream` (default: torch's current stream)."""
+    M, N, dev = _check_inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, mode)
+    _check_dev("out_u", out_u if mode & SL else None, (3, M))
+    _check_dev("out_v", out_v if mode & DL else None, (3, M))
     if mode & SL and out_u is None:
-        out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_u = _out((3, M), dev, stream)
     if mode & DL and out_v is None:
-        out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_v = _out((3, M), dev, stream)
     L = _lib.load()
     if workspace is None:
         if options is None:
-            workspace = alloc_workspace(M, N, mode, dev)
+            workspace = _scratch(workspace_bytes(M, N, mode), dev, stream)
         else:
-            nbytes = int(L.stokes_er_workspace_bytes_ex(M, N, mode, ctypes.byref(options)))
-            workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+            workspace = _scratch(L.stokes_er_workspace_bytes_ex(M, N, mode, ctypes.byref(options)), dev, stream)
     args = [_ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
             _ptr(q if mode & DL else None), _ptr(tgt_xyz), _ptr(tgt_b), _ptr(tgt_x0_density), M, N, float(h),
             _lib.rho_arg(rho), int(mode), _ptr(out_u if mode & SL else None), _ptr(out_v if mode & DL else None),
@@ -144,15 +176,15 @@ def evaluate_host(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_
 def evaluate_onsurface(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, delta, mode=BOTH,
                        out_u=None, out_v=None, workspace=None, stream=None):
     """stokes_er_eval_onsurface (NEXT-1): single delta, s# factors, no extrapolation."""
-    torch = _torch()
-    M, N = _shapes(src_xyz, tgt_b)
-    dev = src_xyz.device
+    M, N, dev = _check_inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, mode)
+    _check_dev("out_u", out_u if mode & SL else None, (3, M))
+    _check_dev("out_v", out_v if mode & DL else None, (3, M))
     if mode & SL and out_u is None:
-        out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_u = _out((3, M), dev, stream)
     if mode & DL and out_v is None:
-        out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_v = _out((3, M), dev, stream)
     if workspace is None:
-        workspace = alloc_workspace(M, N, mode, dev)
+        workspace = _scratch(workspace_bytes(M, N, mode), dev, stream)
     L = _lib.load()
     _lib.check("stokes_er_eval_onsurface", L.stokes_er_eval_onsurface(
         _ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
@@ -165,11 +197,9 @@ def evaluate_onsurface(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tg
 def eval_deltas(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho, mode=BOTH,
                 stream=None):
     """stokes_er_eval_deltas: per-delta u^{delta_k}, v^{delta_k} as (3,3,M) tensors [k][i][m]."""
-    torch = _torch()
-    M, N = _shapes(src_xyz, tgt_b)
-    dev = src_xyz.device
-    ud = torch.empty((3, 3, M), dtype=torch.float64, device=dev) if mode & SL else None
-    vd = torch.empty((3, 3, M), dtype=torch.float64, device=dev) if mode & DL else None
+    M, N, dev = _check_inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, mode)
+    ud = _out((3, 3, M), dev, stream) if mode & SL else None
+    vd = _out((3, 3, M), dev, stream) if mode & DL else None
     L = _lib.load()
     _lib.check("stokes_er_eval_deltas", L.stokes_er_eval_deltas(
         _ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
@@ -180,12 +210,14 @@ def eval_deltas(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_de
 
 def extrapolate(tgt_b, h, rho, in_delta, stream=None):
     """stokes_er_extrapolate: in_delta (3, C, M) device -> (C, M)."""
-    torch = _torch()
     _, C, M = in_delta.shape
-    out = torch.empty((C, M), dtype=torch.float64, device=in_delta.device)
+    _check_dev("tgt_b", tgt_b, (M,))
+    in_delta = in_delta.contiguous()
+    _check_dev("in_delta", in_delta, (3, C, M))
+    out = _out((C, M), in_delta.device, stream)
     L = _lib.load()
     _lib.check("stokes_er_extrapolate", L.stokes_er_extrapolate(
-        _ptr(tgt_b), M, float(h), _lib.rho_arg(rho), _ptr(in_delta.contiguous()), int(C), _ptr(out),
+        _ptr(tgt_b), M, float(h), _lib.rho_arg(rho), _ptr(in_delta), int(C), _ptr(out),
         _stream_handle(stream)))
     return out
 
@@ -325,25 +357,19 @@ class TreePlan:
 def evaluate_tree(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho, plan: TreePlan,
                   mode=BOTH, out_u=None, out_v=None, workspace=None, stream=None):
     """stokes_er_eval_tree on device tensors with a TreePlan over the same nodes."""
-    torch = _torch()
-    M, N = _shapes(src_xyz, tgt_b)
-    dev = src_xyz.device
-    for name, t, shp in (("src_xyz", src_xyz, (3, N)), ("src_normal", src_normal, (3, N)),
-                         ("src_weight", src_weight, (N,)), ("tgt_xyz", tgt_xyz, (3, M)), ("tgt_b", tgt_b, (M,)),
-                         ("tgt_x0_density", tgt_x0_density, (9, M))):
-        _check_dev(name, t, shp)
-    _check_dev("f", f if mode & SL else None, (3, N))
-    _check_dev("q", q if mode & DL else None, (3, N))
+    M, N, dev = _check_inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, mode)
+    _check_dev("out_u", out_u if mode & SL else None, (3, M))
+    _check_dev("out_v", out_v if mode & DL else None, (3, M))
     if plan.N != N:
         raise ValueError("plan built for another node count")
     L = _lib.load()
     if mode & SL and out_u is None:
-        out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_u = _out((3, M), dev, stream)
     if mode & DL and out_v is None:
-        out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_v = _out((3, M), dev, stream)
     if workspace is None:
-        nbytes = int(L.stokes_er_tree_workspace_bytes(M, N, mode, ctypes.byref(plan.params), plan.ptr()))
-        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+        workspace = _scratch(L.stokes_er_tree_workspace_bytes(M, N, mode, ctypes.byref(plan.params), plan.ptr()),
+                             dev, stream)
     st = L.stokes_er_eval_tree(_ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
                                _ptr(q if mode & DL else None), _ptr(tgt_xyz), _ptr(tgt_b), _ptr(tgt_x0_density), M,
                                N, float(h), _lib.rho_arg(rho), int(mode), ctypes.byref(plan.params), plan.ptr(),
@@ -362,19 +388,19 @@ def evaluate_tree_block(block, plan=None, mode=BOTH, device="cuda", leaf_size=20
 def evaluate_tree_onsurface(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, delta,
                             plan: TreePlan, mode=BOTH, out_u=None, out_v=None, workspace=None, stream=None):
     """stokes_er_eval_tree_onsurface: NEXT-1's s# evaluation with the treecode far part."""
-    torch = _torch()
-    M, N = _shapes(src_xyz, tgt_b)
-    dev = src_xyz.device
+    M, N, dev = _check_inputs(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, mode)
+    _check_dev("out_u", out_u if mode & SL else None, (3, M))
+    _check_dev("out_v", out_v if mode & DL else None, (3, M))
     if plan.N != N:
         raise ValueError("plan built for another node count")
     L = _lib.load()
     if mode & SL and out_u is None:
-        out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_u = _out((3, M), dev, stream)
     if mode & DL and out_v is None:
-        out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
+        out_v = _out((3, M), dev, stream)
     if workspace is None:
-        nbytes = int(L.stokes_er_tree_workspace_bytes(M, N, mode, ctypes.byref(plan.params), plan.ptr()))
-        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+        workspace = _scratch(L.stokes_er_tree_workspace_bytes(M, N, mode, ctypes.byref(plan.params), plan.ptr()),
+                             dev, stream)
     st = L.stokes_er_eval_tree_onsurface(_ptr(src_xyz), _ptr(src_normal), _ptr(src_weight),
                                          _ptr(f if mode & SL else None), _ptr(q if mode & DL else None),
                                          _ptr(tgt_xyz), _ptr(tgt_b), _ptr(tgt_x0_density), M, N, float(delta),

@@ -75,20 +75,10 @@ __device__ __forceinline__ void s_factors(double t, double& s1, double& s2, doub
   s3 = s2 - c23;
 }
 
-// On-surface factors s#_i of PAPER.md:130-138 (NEXT-1), same convention.
-__device__ __forceinline__ void s_sharp_factors(double t, double& s1, double& s2, double& s3, double& c23) {
-  const double E = erf(t);
-  const double e = exp(-t * t) * kInvSqrtPi;
-  const double t2 = t * t, t3 = t2 * t, t5 = t3 * t2;
-  s1 = E + (2.0 / 3.0) * (5.0 * t - 2.0 * t3) * e;
-  s2 = E - (2.0 / 3.0) * (3.0 * t - 14.0 * t3 + 4.0 * t5) * e;
-  s3 = E - (2.0 / 9.0) * (9.0 * t + 6.0 * t3 - 4.0 * t5) * e;
-  c23 = s2 - s3;
-}
-
-// e^{-u} for 0 <= u <= 700 (near pairs: u <= 144): Cody-Waite reduction
-// u = n ln2 + r, |r| <= ln2/2, degree-11 polynomial (tools/gen_sfactor_coeffs.py),
-// scale 2^n by building the exponent bits.  No special-case branches.
+// e^{-u} for 0 <= u <= 700: Cody-Waite reduction u = n ln2 + r, |r| <= ln2/2,
+// degree-11 polynomial (tools/gen_sfactor_coeffs.py), scale 2^n by building the
+// exponent bits.  No special-case branches; u > ~708 would overflow the exponent
+// field, so callers clamp u (e^{-700} ~ 1e-304 is below every contribution).
 __device__ __forceinline__ double exp_neg(double u) {
   const double x = -u;
   const double kd = fma(x, 1.4426950408889634074, 6755399441055744.0);  // round(x/ln2) + 1.5*2^52
@@ -118,7 +108,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // Branch-free, no tables; for t < 0.5 it returns finite values the caller discards.
 __device__ __forceinline__ void sfactor_s(double t, double& E, double& s2, double& c23, double* e_out = nullptr) {
   const double u = t * t;
-  const double e = exp_neg(u);
+  // t = r/delta_k can reach 6 rho_3/rho_1 on a near pair (t^2 > 700 once
+  // rho_3/rho_1 > 4.4): clamp so exp_neg stays in range; e^{-700} is 0 to the sums
+  const double e = exp_neg(fmin(u, 700.0));
   if (e_out) *e_out = e;  // e^{-t^2}, for callers that need it too (the s# factors)
   const double tc = fmin(t, 6.0);  // erfc(t > 6) < 2e-17: E rounds to 1 either way
   const double x = fma(rcp_nr(kErfcxKappa + tc), kErfcxVA, kErfcxVB);

@@ -474,7 +474,7 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   tfp.n_groups = static_cast<int>(P.Mpad / 32);
   tfp.p = p;
   tfp.theta = tp->theta;
-  tfp.rc2 = rc2;
+  tfp.rc2 = rc2 * (1.0 + 1e-9);  // R23 guard with the rc2_box margin: no pair the near units own is approximated
   NearParams np;
   np.src = src;
   np.src_box = srcbox;

@@ -281,7 +281,7 @@ struct TreeFarParams {
   int* counter;
   int64_t Mpad;
   int n_groups, p;
-  double theta, rc2;      // MAC parameter, (c delta_max)^2
+  double theta, rc2;      // MAC parameter, guard (c delta_max)^2 (1 + 1e-9)
 };
 
 struct __align__(16) TreeWarpSmem {

@@ -14,8 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 def test_bench_json_line():
-    r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"],
-                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    r = subprocess.run([sys.executable, "bench.py", "--config", "5", "--inv-h", "64", "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [json.loads(s) for s in r.stdout.splitlines() if s.startswith("{")]
     assert len(lines) == 1
@@ -31,7 +31,10 @@ def test_bench_json_line():
     assert d["gpu_launches"] > 0
     e2e = d["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
-    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"] and d["clocks"]["samples"] >= 3
+    par = d["parity"]  # sampled parity against the oracle's definition mode, and the solve alone
+    assert par["u_max_rel"] <= 1e-12 and par["v_max_rel"] <= 1e-12 and par["solve_max_rel"] <= 1e-13
+    assert d["config"]["workload"] == "cfg5_sphere_h1/64"
 
 
 @pytest.mark.gpu

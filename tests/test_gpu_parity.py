@@ -436,3 +436,16 @@ def test_randomized_parity_sweep(ser, tmp_path):
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     assert mod.main(str(tmp_path / "sweep.json"), 40) == 0
+
+
+@pytest.mark.parametrize("rho", [(1.0, 2.0, 5.0), (1.0, 3.0, 8.0)])
+def test_wide_rho_ratio(ser, rho):
+    """rho_3 / rho_1 > 4.4: a near pair (r <= 6 delta_3) reaches t_1 = r/delta_1 = 6 rho_3/rho_1
+    > 26.6, where t_1^2 > 700 would overflow the CUDA path's exp unless its argument is clamped
+    (device_math.cuh sfactor_s).  Every pair of config 2 at 1/h = 16 is compared with the
+    oracle's definition mode (libm exp underflows to 0 there)."""
+    import dataclasses
+
+    blk = config2(inv_h=16)
+    blk = dataclasses.replace(blk, rho=tuple(rho)).take_targets(np.arange(0, blk.M, 2))
+    check_block(ser, blk, localized=False)

@@ -92,3 +92,57 @@ def test_morton_order_is_a_local_permutation():
     assert sorted(p.tolist()) == list(range(blk.M))
     step = lambda perm: float((x[:, perm[1:]] - x[:, perm[:-1]]).norm(dim=0).mean())
     assert step(p) < 0.25 * step(torch.arange(blk.M))  # config 2 lists nodes, then a random shell
+
+
+def _bench_worker(rank, world, port, out_dir):
+    """bench.py's multi-rank arm: its step goes through sharding.evaluate_sharded on ONE
+    target set (the rank-0 seed on every rank) and gathers the full field."""
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    import oracle
+    from paper_2507_00156_b200 import sharding
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    calls = []
+    real = sharding.evaluate_sharded
+
+    def spy(*a, **kw):
+        calls.append(kw.get("gather"))
+        return real(*a, **kw)
+
+    sharding.evaluate_sharded = spy
+    blk = bench.make_workload(1, 16, 0)  # what run_eval builds on every rank (strong scaling)
+    seen = []
+
+    def oracle_fn(sx, sn, sw, f, q, ty, tb, tx, h, rho, mode=3):
+        seen.append(int(tb.shape[0]))
+        u, v = oracle.evaluate(*(a.numpy() for a in (sx, sn, sw, f, q, ty, tb, tx)), h, rho, mode=mode)
+        return torch.from_numpy(u), torch.from_numpy(v)
+
+    u, v = bench.sharded_step([torch.from_numpy(a) for a in blk.arrays()], blk, oracle_fn)
+    assert calls == [True] and seen == [sharding.shard_bounds(blk.M, rank, world)[1]
+                                        - sharding.shard_bounds(blk.M, rank, world)[0]]
+    if rank == 0:
+        np.save(os.path.join(out_dir, "bu.npy"), u.numpy())
+        np.save(os.path.join(out_dir, "bv.npy"), v.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_multirank_arm_goes_through_evaluate_sharded(tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle
+    sys.path.insert(0, ROOT)
+    import bench
+
+    oracle.build()
+    port = _free_port()
+    mp.spawn(_bench_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    blk = bench.make_workload(1, 16, 0)
+    u_ref, v_ref = oracle.evaluate_block(blk)
+    np.testing.assert_array_equal(np.load(tmp_path / "bu.npy"), u_ref)
+    np.testing.assert_array_equal(np.load(tmp_path / "bv.npy"), v_ref)

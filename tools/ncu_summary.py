@@ -1,7 +1,11 @@
 #!/usr/bin/env python
 """Summarise an ncu report (.ncu-rep) into profiles/: key metrics per kernel as JSON.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01/ncu_xxx.json
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r02/ncu_full_xxx.json [bench_line.json]
+
+With a bench line (the JSON bench.py printed for the SAME arguments without ncu), the
+summary records that run's configuration as "bench_config"; bench.py takes
+roofline.traffic only from a summary whose bench_config equals its own run.
 """
 from __future__ import annotations
 
@@ -28,7 +32,15 @@ KEYS = [
 STALL_PREFIX = "smsp__average_warps_issue_stalled_"
 
 
-def main(rep, out):
+def bench_config(path):
+    for line in open(path):
+        if line.startswith("{"):
+            c = json.loads(line)["config"]
+            return {k: c.get(k) for k in ("workload", "path", "schedule", "targets_per_thread")}
+    return None
+
+
+def main(rep, out, bench_line=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -55,10 +67,14 @@ def main(rep, out):
         except (ValueError, IndexError):
             pass
         res.append(k)
+    doc = {"report": rep, "kernels": res}
+    if bench_line:
+        doc["bench_config"] = bench_config(bench_line)
+        doc["bench_line"] = bench_line
     with open(out, "w") as fh:
-        json.dump({"report": rep, "kernels": res}, fh, indent=1)
+        json.dump(doc, fh, indent=1)
     print(json.dumps(res, indent=1)[:3000])
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
