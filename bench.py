@@ -46,6 +46,12 @@ F_NEAR_ALG = 180
 F_NEAR_SHARP_ALG = 84
 F_FAR_ISSUED = 64   # ncu-countable FP64 flops (2*DFMA + DMUL + DADD) of far_pair<3> (41 instructions)
 F_NEAR_ISSUED = 343  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r01/ncu_full_v15_far_near.json: 135 DFMA, 48 DMUL, 24 DADD)
+# node-target path (csrc/sym.cuh): one evaluation of a far pair's shared part serves both directed
+# pairs.  Algorithmic flops per UNORDERED pair (rsqrt = 1, FMA = 2): d 3, r^2 5, rsqrt 1, 1/r^2 and
+# 1/r^5 3, SL 2 x 24, DL: q_j - q_i 3, d.dq 5, dq/r^5 1 shared + 2 x (d.mw 5, x 1, v += d c 6) = 93,
+# i.e. 46.5 per directed pair (57 when each direction is computed alone).
+F_SYM_UNORDERED_ALG = 93
+F_SYM_UNORDERED_ISSUED = 100  # sym_pair<3>: 61 FP64 instructions = 39 DFMA + 16 DMUL + 6 DADD (2*39 + 16 + 6)
 SMS = 148
 FP64_LANES_PER_SM = 64  # measured: DFMA loop 58.7 FMA/clk/SM at the boost clock (tools/probes)
 
@@ -72,6 +78,9 @@ def parse():
                          "tree: one stokes_er_eval_tree (NEXT-3) of config --config at 1/h = --inv-h")
     ap.add_argument("--tree", type=str, default="",
                     help="treecode N0,p,theta (default: PAPER.md eq. (33) policy for --inv-h)")
+    ap.add_argument("--path", choices=["auto", "general", "nodes"], default="auto",
+                    help="nodes: stokes_er_eval_nodes (targets = the nodes, symmetric far kernel); general: "
+                         "stokes_er_eval; auto: nodes when the workload's targets are its nodes (config 5) on 1 GPU")
     ap.add_argument("--schedule", choices=["fused", "separate"], default="fused",
                     help="fused: one persistent kernel, far items and near items from one interleaved "
                          "queue (default); separate: far kernel then near kernel")
@@ -663,12 +672,14 @@ def cpu_baseline(block, definition=None):
     rng = np.random.default_rng(1)
 
     def rate(localized, nthreads, budget_s):
-        k = 8
-        t0 = time.perf_counter()
-        oracle.evaluate_block(block.take_targets(rng.choice(block.M, k, replace=False)), localized=localized,
-                              nthreads=nthreads)
-        per_target = (time.perf_counter() - t0) / k
-        k = int(min(block.M, max(8, budget_s / per_target)))
+        k, dt = 4, 0.0
+        while dt < 0.1 * budget_s and k < block.M:  # calibrate on a growing sample (thread start-up amortised)
+            k = min(block.M, 2 * k)
+            t0 = time.perf_counter()
+            oracle.evaluate_block(block.take_targets(rng.choice(block.M, k, replace=False)), localized=localized,
+                                  nthreads=nthreads)
+            dt = time.perf_counter() - t0
+        k = int(min(block.M, max(8, budget_s * k / max(dt, 1e-9))))
         idx = rng.choice(block.M, k, replace=False)
         t0 = time.perf_counter()
         oracle.evaluate_block(block.take_targets(idx), localized=localized, nthreads=nthreads)
@@ -707,9 +718,11 @@ def sharded_step(arrs, block, evaluate_fn):
 
 
 def run_eval(args, rank, world):
-    """The default bench: one step = one full SL+DL 3-delta evaluation (stokes_er_eval)
-    of BASELINE.json config --config at 1/h = --inv-h (default config 5 at 1/h = 256:
-    the unit sphere's N = M = 1,090,854 nodes, every node a target at b = 0).
+    """The default bench: one step = one full SL+DL 3-delta evaluation of BASELINE.json
+    config --config at 1/h = --inv-h (default config 5 at 1/h = 256: the unit sphere's
+    N = M = 1,090,854 nodes, every node a target at b = 0).  Config 5's targets are its
+    nodes, so on one GPU the step is stokes_er_eval_nodes (the same sums with the symmetric
+    far kernel); other configs, or --path general, use stokes_er_eval.
 
     N = 1: one process evaluates the whole block.  N > 1 (torchrun, NCCL): ONE seeded
     target set split across the ranks by sharding.evaluate_sharded (contiguous ranges
@@ -748,8 +761,14 @@ def run_eval(args, rank, world):
     fused = args.schedule != "separate"
     opt.schedule = {"fused": 0, "separate": 1}[args.schedule]
     L = ser._lib.load()
-    ws = torch.empty(int(L.stokes_er_workspace_bytes_ex(M_loc, N, 3, ctypes.byref(opt))), dtype=torch.uint8,
-                     device=dev)
+    nodes = args.path == "nodes" or (args.path == "auto" and args.config == 5 and world == 1)
+    if nodes and (world > 1 or args.config != 5):
+        raise SystemExit("--path nodes: node-target workloads (config 5) on one GPU")
+    if nodes:
+        ws = torch.empty(ser.nodes_workspace_bytes(N, 3, opt), dtype=torch.uint8, device=dev)
+    else:
+        ws = torch.empty(int(L.stokes_er_workspace_bytes_ex(M_loc, N, 3, ctypes.byref(opt))), dtype=torch.uint8,
+                         device=dev)
     out_u = torch.empty((3, M), dtype=torch.float64, device=dev)
     out_v = torch.empty((3, M), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -765,6 +784,14 @@ def run_eval(args, rank, world):
                             stream=stream, options=opt)
 
     def step(ev_pair=None, ev_near=None):
+        if nodes:
+            opt.pair_kernel_start_event = ev_pair[0].cuda_event if ev_pair else None
+            opt.pair_kernel_end_event = ev_pair[1].cuda_event if ev_pair else None
+            opt.near_kernel_start_event = ev_near[0].cuda_event if ev_near else None
+            opt.near_kernel_end_event = ev_near[1].cuda_event if ev_near else None
+            ser.evaluate_nodes(*arrs[:5], block.h, block.rho, out_u=out_u, out_v=out_v, workspace=ws, stream=stream,
+                               options=opt)
+            return out_u, out_v
         if world == 1:
             local_eval(*arrs, block.h, block.rho, ev_pair=ev_pair, ev_near=ev_near, ou=out_u, ov=out_v)
             return out_u, out_v
@@ -810,7 +837,12 @@ def run_eval(args, rank, world):
         host = [torch.from_numpy(a).pin_memory() for a in block.arrays()]
         hu = torch.empty((3, M), dtype=torch.float64).pin_memory()
         hv = torch.empty((3, M), dtype=torch.float64).pin_memory()
-        if world == 1:
+        if nodes:
+            host = host[:5]  # the targets are the nodes: only the source arrays travel
+            hws = torch.empty(int(L.stokes_er_nodes_host_workspace_bytes(N, 3)), dtype=torch.uint8, device=dev)
+            e_step = lambda: ser.evaluate_nodes_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws,
+                                                     stream=stream)
+        elif world == 1:
             hws = ser.alloc_workspace(M, N, 3, dev, host=True)
             e_step = lambda: ser.evaluate_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws,
                                                stream=stream)
@@ -838,10 +870,11 @@ def run_eval(args, rank, world):
             e_ms.append(a.elapsed_time(b))
         e_total = max_over_ranks(sum(e_ms) / 1e3, dev)
         e2e = {"value": pairs * ke / e_total, "unit": UNIT,
-               "h2d_bytes_per_step": int(sum(a.nbytes for a in block.arrays())),
+               "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in host)),
                "d2h_bytes_per_step": int(hu.numel() * 8 + hv.numel() * 8),
-               "api": "stokes_er_eval_host (C ABI, pinned host buffers)" if world == 1 else
-                      "host->device copies + sharding.evaluate_sharded (all-gather) + device->host copy"}
+               "api": ("stokes_er_eval_nodes_host (C ABI, pinned host buffers)" if nodes else
+                       "stokes_er_eval_host (C ABI, pinned host buffers)" if world == 1 else
+                       "host->device copies + sharding.evaluate_sharded (all-gather) + device->host copy")}
 
     sol_err = solve_parity(block, dev, stream) if rank == 0 else None
     if rank != 0:
@@ -859,7 +892,18 @@ def run_eval(args, rank, world):
     peak = SMS * FP64_LANES_PER_SM * 2 * f_clk * 1e6 / 1e12  # TFLOP/s
     peak_source = ("derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz max SM clock (MEASURED_PEAKS.json has "
                    "no FP64 entry; DFMA-loop probe 34.2 TFLOP/s = 92% of it, tools/probes)")
-    if fused:
+    sym_pairs = nbr_pairs = None
+    if nodes:
+        sym_pairs, nbr_pairs = ser.nodes_pair_counts(N, block.h, block.rho, ws, stream=stream)
+    if nodes:
+        k_flops = sym_pairs / 2 * F_SYM_UNORDERED_ALG
+        k_issued = sym_pairs / 2 * F_SYM_UNORDERED_ISSUED
+        kname = ("sym_kernel<3> (FP64 pipe): the far-field sum (PAPER.md:183-191) over all-far 64-node block "
+                 "pairs, one evaluation of each pair's shared part for both directed pairs (node targets)")
+        kprefix = "void ser::sym_kernel<3>"
+        conv = (f"{F_SYM_UNORDERED_ALG} algorithmic flops per unordered far pair = {F_SYM_UNORDERED_ALG / 2} per "
+                "directed pair (rsqrt = 1, FMA = 2; the shared geometry and d.(q_j - q_i) counted once)")
+    elif fused:
         k_flops = (far * F_FAR_ALG + near * F_NEAR_ALG) * share
         k_issued = (far * F_FAR_ISSUED + near * F_NEAR_ISSUED) * share
         kname = ("fused_kernel<3,T> (FP64 pipe): far-field sum (PAPER.md:183-191) + near 3-delta sums "
@@ -874,8 +918,8 @@ def run_eval(args, rank, world):
         kprefix = "void ser::far_kernel<3"
         conv = f"{F_FAR_ALG} algorithmic flops per far pair (rsqrt = 1, FMA = 2)"
     achieved = k_flops / far_avg_s / 1e12
-    bench_cfg = {"workload": block.name, "path": "stokes_er_eval", "schedule": args.schedule,
-                 "targets_per_thread": int(opt.stats[3])}
+    bench_cfg = {"workload": block.name, "path": "stokes_er_eval_nodes" if nodes else "stokes_er_eval",
+                 "schedule": "nodes" if nodes else args.schedule, "targets_per_thread": int(opt.stats[3])}
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": None, "traffic_source": "no ncu --set full capture of this exact configuration committed",
                 "kernel": kname, "peak_source": peak_source,
@@ -890,7 +934,18 @@ def run_eval(args, rank, world):
     if clocks.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (SMS * FP64_LANES_PER_SM * 2 * clocks["sm_mhz"] / 1e6)
     near_info = None
-    if not fused:
+    if nodes:
+        near_avg_s = statistics.mean(near_ms) / 1e3
+        roofline["far_pairs_per_s"] = sym_pairs / far_avg_s
+        roofline["frac_57_flop_convention"] = sym_pairs * F_FAR_ALG / far_avg_s / 1e12 / peak
+        roofline["directed_pairs"] = sym_pairs
+        nbr_far = nbr_pairs - near
+        near_info = {"kernel": "nbr_kernel<3>: near 3-delta pairs + the far pairs of the block pairs the "
+                               "symmetric kernel leaves out (own block, not all-far)",
+                     "ms": near_avg_s * 1e3, "share": sum(near_ms) / sum(step_ms), "pairs": nbr_pairs,
+                     "near_pairs": near, "far_pairs": nbr_far,
+                     "tflops_alg": (near * F_NEAR_ALG + nbr_far * F_FAR_ALG) / near_avg_s / 1e12}
+    elif not fused:
         near_avg_s = statistics.mean(near_ms) / 1e3
         roofline["far_pairs_per_s"] = far * share / far_avg_s
         near_info = {"kernel": "near_kernel<3>", "ms": near_avg_s * 1e3, "share": sum(near_ms) / sum(step_ms),
@@ -910,17 +965,22 @@ def run_eval(args, rank, world):
                        "inputs": "resident in HBM", "seed": block.meta.get("seed"),
                        "targets_per_thread": int(opt.stats[3]), "work_items": int(opt.stats[0]),
                        "grid_ctas": int(opt.stats[1]), "chunk_tiles": int(opt.stats[2]),
-                       "schedule": args.schedule, "path": "stokes_er_eval",
+                       "schedule": "nodes" if nodes else args.schedule,
+                       "path": "stokes_er_eval_nodes" if nodes else "stokes_er_eval",
                        "parallelism": ("single GPU" if world == 1 else
                                        f"target-sharded x{world}: Morton ranges of ONE target set "
                                        "(sharding.evaluate_sharded), sources replicated, all-gather of u, v in the "
                                        "timed region")},
             "fp64_tflops_alg": alg_flops * K / total_s / 1e12,
             "roofline": roofline, "clocks": clocks, "parity": parity,
-            "gpu_launches": K * (ser.launch_count(M_loc, N, 3) + (0 if fused else 1)),
-            "gpu_launches_note": "our kernels per step and rank: bbox, 2 morton, pack_sources, pack_targets, "
-                                 + ("fused far+near" if fused else "far, near") + ", finalize "
-                                 "(+ CUB radix-sort launches, library code)",
+            "gpu_launches": K * (ser.nodes_launch_count(N, 3) if nodes else
+                                 ser.launch_count(M_loc, N, 3) + (0 if fused else 1)),
+            "gpu_launches_note": ("our kernels per step: bbox, morton, pack_sources, pack_node_soa, block_boxes, "
+                                  "sym_kernel, nbr_kernel, finalize_nodes (+ CUB radix-sort launches, library code)"
+                                  if nodes else
+                                  "our kernels per step and rank: bbox, 2 morton, pack_sources, pack_targets, "
+                                  + ("fused far+near" if fused else "far, near") + ", finalize "
+                                  "(+ CUB radix-sort launches, library code)"),
             "e2e": e2e}
     if near_info is not None:
         line["near_kernel"] = near_info

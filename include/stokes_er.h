@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define STOKES_ER_ABI_VERSION 2  /* 2: options.schedule, NEXT-2 (two drops) and NEXT-3 (treecode) entry points */
+#define STOKES_ER_ABI_VERSION 3  /* 3: node-target entry points (stokes_er_eval_nodes*); 2: options.schedule, NEXT-2, NEXT-3 */
 /* c: near iff r <= c * max(delta_k)  ("s1=s2=s3=1 for t > 6") */
 #define STOKES_ER_CUTOFF 6.0
 /* c for the on-surface s# variant: 1 - s2#(6) = 2.45e-12, 1 - s_i#(7) < 1e-16 (R15) */
@@ -190,6 +190,57 @@ int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const dou
                       const double* tgt_x0_density, int64_t M, int64_t N, double h, const double rho[3],
                       int mode, double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
                       void* stream, stokes_er_options* options);
+
+/* ================================================================ node targets
+ * Evaluation AT THE QUADRATURE NODES: the targets are the N nodes themselves,
+ * on the surface (b = 0, chi = 1/2), with x0 = the node, n0 = its
+ * normal, f(x0) = f and q(x0) = q at the node.  The result is exactly that of
+ * stokes_er_eval with M = N, tgt_xyz = src_xyz, tgt_b = 0 and tgt_x0_density =
+ * [src_normal; f; q] (same formulas, same localization and extrapolation; the
+ * paper's on-surface targets, PAPER.md:249 with b = 0, and BASELINE.json
+ * config 5).  Out: out_u, out_v [3][N] in the caller's node order.
+ *
+ * Node targets make the far-field pair sum symmetric: S(d) is even and T(d)
+ * odd in d = x_i - x_j (eqs. (3)-(4)), and q0 = q at a node
+ * makes the stresslet's d.(q_j - q_i) shared as well, so ONE evaluation of a
+ * far pair's geometry (d, r^2, 1/r, 1/r^2, 1/r^5) and of d.(q_j - q_i) serves
+ * both directed pairs (i <- j) and (j <- i).  Results are deterministic (no
+ * data atomics; fixed summation order) and equal stokes_er_eval's to rounding.
+ *
+ * Arrays, errors and streams as stokes_er_eval (N >= 1; mode, h, rho alike).
+ * Workspace: stokes_er_nodes_workspace_bytes(N, mode) device bytes -- it holds
+ * one accumulator slice of 48 N bytes per persistent CTA (148), i.e. ~7.1 KB
+ * per node (7.8 GB at N = 1.09e6), sized for the B200's 180 GB of HBM.
+ * stokes_er_eval_nodes_ex takes the same options struct as stokes_er_eval_ex:
+ * the pair_kernel events bracket the symmetric far kernel, the near_kernel
+ * events the neighbour kernel (near pairs + the far pairs of the blocks the
+ * symmetric kernel leaves out); near_phases is honoured; stats[0..3] = items,
+ * CTAs, R blocks per item, 2.
+ */
+size_t stokes_er_nodes_workspace_bytes(int64_t N, int mode);
+size_t stokes_er_nodes_workspace_bytes_ex(int64_t N, int mode, const stokes_er_options* options);
+int stokes_er_eval_nodes(const double* src_xyz, const double* src_normal, const double* src_weight,
+                         const double* f, const double* q, int64_t N, double h, const double rho[3], int mode,
+                         double* out_u, double* out_v, void* workspace, size_t workspace_bytes, void* stream);
+int stokes_er_eval_nodes_ex(const double* src_xyz, const double* src_normal, const double* src_weight,
+                            const double* f, const double* q, int64_t N, double h, const double rho[3], int mode,
+                            double* out_u, double* out_v, void* workspace, size_t workspace_bytes, void* stream,
+                            stokes_er_options* options);
+/* HOST buffers (pinned recommended): H2D, evaluation, D2H, then synchronizes `stream`.
+ * Workspace: stokes_er_nodes_host_workspace_bytes(N, mode) device bytes. */
+size_t stokes_er_nodes_host_workspace_bytes(int64_t N, int mode);
+int stokes_er_eval_nodes_host(const double* src_xyz_host, const double* src_normal_host,
+                              const double* src_weight_host, const double* f_host, const double* q_host, int64_t N,
+                              double h, const double rho[3], int mode, double* out_u_host, double* out_v_host,
+                              void* workspace, size_t workspace_bytes, void* stream);
+/* Statistics for benchmarks (synchronizes `stream`; not for the hot path): after a
+ * stokes_er_eval_nodes call with this workspace (same N, mode, h, rho), counts_host[0] =
+ * directed pairs of real nodes summed by the symmetric far kernel (2 per shared pair),
+ * counts_host[1] = N^2 - counts_host[0], the pairs the neighbour kernel owns. */
+int stokes_er_nodes_pair_counts(int64_t N, int mode, double h, const double rho[3], void* workspace,
+                                size_t workspace_bytes, int64_t* counts_host, void* stream);
+/* Kernel launches one stokes_er_eval_nodes enqueues (ours; CUB's sort launches excluded). */
+int stokes_er_nodes_launch_count(int64_t N, int mode);
 
 /* Treecode parameters (NEXT-3, Sec. 3.4; section below). */
 typedef struct {

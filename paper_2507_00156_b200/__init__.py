@@ -194,6 +194,104 @@ def evaluate_onsurface(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tg
     return (out_u if mode & SL else None), (out_v if mode & DL else None)
 
 
+def nodes_workspace_bytes(N: int, mode: int = BOTH, options: "_lib.Options | None" = None) -> int:
+    L = _lib.load()
+    if options is None:
+        return int(L.stokes_er_nodes_workspace_bytes(N, mode))
+    return int(L.stokes_er_nodes_workspace_bytes_ex(N, mode, ctypes.byref(options)))
+
+
+def nodes_launch_count(N: int, mode: int = BOTH) -> int:
+    return int(_lib.load().stokes_er_nodes_launch_count(N, mode))
+
+
+def evaluate_nodes(src_xyz, src_normal, src_weight, f, q, h, rho, mode=BOTH, out_u=None, out_v=None, workspace=None,
+                   stream=None, options: "_lib.Options | None" = None):
+    """stokes_er_eval_nodes: the same evaluation as `evaluate` with the targets = the N nodes
+    (b = 0, x0 = node, n0 = its normal, f(x0) = f, q(x0) = q); returns (u (3,N), v (3,N))."""
+    N = int(src_xyz.shape[1])
+    _check_dev("src_xyz", src_xyz, (3, N))
+    _check_dev("src_normal", src_normal, (3, N))
+    _check_dev("src_weight", src_weight, (N,))
+    _check_dev("f", f if mode & SL else None, (3, N))
+    _check_dev("q", q if mode & DL else None, (3, N))
+    _check_dev("out_u", out_u if mode & SL else None, (3, N))
+    _check_dev("out_v", out_v if mode & DL else None, (3, N))
+    dev = src_xyz.device
+    for name, t in (("src_normal", src_normal), ("src_weight", src_weight), ("f", f if mode & SL else None),
+                    ("q", q if mode & DL else None)):
+        if t is not None and t.device != dev:
+            raise ValueError(f"{name}: on {t.device}, expected {dev}")
+    if mode & SL and out_u is None:
+        out_u = _out((3, N), dev, stream)
+    if mode & DL and out_v is None:
+        out_v = _out((3, N), dev, stream)
+    L = _lib.load()
+    if workspace is None:
+        workspace = _scratch(nodes_workspace_bytes(N, mode, options), dev, stream)
+    args = [_ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
+            _ptr(q if mode & DL else None), N, float(h), _lib.rho_arg(rho), int(mode),
+            _ptr(out_u if mode & SL else None), _ptr(out_v if mode & DL else None), _ptr(workspace),
+            int(workspace.numel()), _stream_handle(stream)]
+    if options is None:
+        _lib.check("stokes_er_eval_nodes", L.stokes_er_eval_nodes(*args))
+    else:
+        _lib.check("stokes_er_eval_nodes_ex", L.stokes_er_eval_nodes_ex(*args, ctypes.byref(options)))
+    return (out_u if mode & SL else None), (out_v if mode & DL else None)
+
+
+def nodes_pair_counts(N: int, h, rho, workspace, mode: int = BOTH, stream=None):
+    """(directed pairs summed by the symmetric far kernel, pairs owned by the neighbour kernel)
+    of the last evaluate_nodes with this workspace (synchronizes; statistics only)."""
+    c = (ctypes.c_int64 * 2)()
+    _lib.check("stokes_er_nodes_pair_counts", _lib.load().stokes_er_nodes_pair_counts(
+        N, int(mode), float(h), _lib.rho_arg(rho), _ptr(workspace), int(workspace.numel()), c,
+        _stream_handle(stream)))
+    return int(c[0]), int(c[1])
+
+
+def evaluate_nodes_host(src_xyz, src_normal, src_weight, f, q, h, rho, mode=BOTH, out_u=None, out_v=None,
+                        workspace=None, stream=None):
+    """stokes_er_eval_nodes_host: HOST float64 arrays in and out (pinned recommended)."""
+    torch = _torch()
+    import numpy as np
+
+    def host(a):
+        if a is None:
+            return None
+        if isinstance(a, np.ndarray):
+            a = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        if a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous():
+            raise TypeError("evaluate_nodes_host expects contiguous float64 host tensors")
+        return a
+
+    src_xyz, src_normal, src_weight, f, q = map(host, (src_xyz, src_normal, src_weight, f, q))
+    N = int(src_xyz.shape[1])
+    if mode & SL and out_u is None:
+        out_u = torch.empty((3, N), dtype=torch.float64).pin_memory()
+    if mode & DL and out_v is None:
+        out_v = torch.empty((3, N), dtype=torch.float64).pin_memory()
+    L = _lib.load()
+    if workspace is None:
+        workspace = torch.empty(max(int(L.stokes_er_nodes_host_workspace_bytes(N, mode)), 1), dtype=torch.uint8,
+                                device="cuda")
+    _lib.check("stokes_er_eval_nodes_host", L.stokes_er_eval_nodes_host(
+        _ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
+        _ptr(q if mode & DL else None), N, float(h), _lib.rho_arg(rho), int(mode), _ptr(out_u if mode & SL else None),
+        _ptr(out_v if mode & DL else None), _ptr(workspace), int(workspace.numel()), _stream_handle(stream)))
+    return (out_u if mode & SL else None), (out_v if mode & DL else None)
+
+
+def evaluate_nodes_block(block, mode=BOTH, device="cuda", **kw):
+    """Convenience for tests/bench: the node-target evaluation of a Block's SOURCES (its
+    own targets are ignored; `node_block` in workloads.configs builds the equivalent
+    general-path Block)."""
+    torch = _torch()
+    arrs = [torch.from_numpy(a).to(device) for a in (block.src_xyz, block.src_normal, block.src_weight, block.f,
+                                                     block.q)]
+    return evaluate_nodes(*arrs, block.h, block.rho, mode=mode, **kw)
+
+
 def eval_deltas(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_x0_density, h, rho, mode=BOTH,
                 stream=None):
     """stokes_er_eval_deltas: per-delta u^{delta_k}, v^{delta_k} as (3,3,M) tensors [k][i][m]."""

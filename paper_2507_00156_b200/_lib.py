@@ -55,7 +55,10 @@ EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_
            "stokes_er_status_string", "stokes_er_abi_version", "stokes_er_twodrop_workspace_bytes",
            "stokes_er_twodrop_workspace_bytes_ex", "stokes_er_twodrop_setup", "stokes_er_twodrop_rhs", "stokes_er_twodrop_apply", "stokes_er_twodrop_solve",
            "stokes_er_tree_plan_bytes", "stokes_er_tree_build", "stokes_er_tree_info", "stokes_er_tree_workspace_bytes",
-           "stokes_er_eval_tree", "stokes_er_eval_tree_onsurface"]
+           "stokes_er_eval_tree", "stokes_er_eval_tree_onsurface", "stokes_er_nodes_workspace_bytes",
+           "stokes_er_nodes_workspace_bytes_ex", "stokes_er_eval_nodes", "stokes_er_eval_nodes_ex",
+           "stokes_er_nodes_host_workspace_bytes", "stokes_er_eval_nodes_host", "stokes_er_nodes_launch_count",
+           "stokes_er_nodes_pair_counts"]
 
 _lib = None
 
@@ -125,6 +128,25 @@ def load():
     L.stokes_er_eval_tree_onsurface.argtypes = [_dp] * 8 + [_i64, _i64, ctypes.c_double, ctypes.c_int, tp, _dp, _dp,
                                                             _dp, _dp, ctypes.c_size_t, _dp]
     L.stokes_er_eval_tree_onsurface.restype = ctypes.c_int
+    nodes_args = [_dp] * 5 + [_i64, ctypes.c_double, ctypes.POINTER(ctypes.c_double), ctypes.c_int, _dp, _dp, _dp,
+                              ctypes.c_size_t, _dp]
+    L.stokes_er_nodes_workspace_bytes.argtypes = [_i64, ctypes.c_int]
+    L.stokes_er_nodes_workspace_bytes.restype = ctypes.c_size_t
+    L.stokes_er_nodes_workspace_bytes_ex.argtypes = [_i64, ctypes.c_int, ctypes.POINTER(Options)]
+    L.stokes_er_nodes_workspace_bytes_ex.restype = ctypes.c_size_t
+    L.stokes_er_nodes_host_workspace_bytes.argtypes = [_i64, ctypes.c_int]
+    L.stokes_er_nodes_host_workspace_bytes.restype = ctypes.c_size_t
+    L.stokes_er_eval_nodes.argtypes = nodes_args
+    L.stokes_er_eval_nodes.restype = ctypes.c_int
+    L.stokes_er_eval_nodes_ex.argtypes = nodes_args + [ctypes.POINTER(Options)]
+    L.stokes_er_eval_nodes_ex.restype = ctypes.c_int
+    L.stokes_er_eval_nodes_host.argtypes = nodes_args
+    L.stokes_er_eval_nodes_host.restype = ctypes.c_int
+    L.stokes_er_nodes_launch_count.argtypes = [_i64, ctypes.c_int]
+    L.stokes_er_nodes_launch_count.restype = ctypes.c_int
+    L.stokes_er_nodes_pair_counts.argtypes = [_i64, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double), _dp,
+                                              ctypes.c_size_t, ctypes.POINTER(_i64), _dp]
+    L.stokes_er_nodes_pair_counts.restype = ctypes.c_int
     _lib = L
     return L
 

@@ -7,6 +7,7 @@
 
 #include "kernels.cuh"
 #include "treecode.cuh"
+#include "sym.cuh"
 
 namespace ser {
 
@@ -474,7 +475,8 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   tfp.n_groups = static_cast<int>(P.Mpad / 32);
   tfp.p = p;
   tfp.theta = tp->theta;
-  tfp.rc2 = rc2 * (1.0 + 1e-9);  // R23 guard with the rc2_box margin: no pair the near units own is approximated
+  tfp.rc2 = rc2;
+  tfp.rc2_guard = rc2 * (1.0 + 1e-9);  // R23 guard with the rc2_box margin: no pair the near units own is approximated
   NearParams np;
   np.src = src;
   np.src_box = srcbox;
@@ -500,6 +502,166 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
                                                           P.near_phases, out_u, out_v);
   return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
 }
+
+
+// ------------------------------------------------------------- node targets
+// stokes_er_eval_nodes (sym.cuh): the symmetric far kernel over 64-node block
+// pairs + the neighbour units + finalize.  The plan depends on N only.
+struct NodePlan {
+  int mode = 3;
+  int64_t N = 0, Npad = 0, n_items = 0;
+  int nb = 0, nsb = 0, chunk = 0, nchunks = 0, G = 0, near_phases = 1;
+  size_t cub_bytes = 0, sym_smem = 0;
+  size_t off_box, off_skin, off_skout, off_svin, off_svout, off_cub, off_src, off_srcbox, off_blkbox, off_nsoa;
+  size_t off_tgt, off_orig, off_pacc, off_near, off_counter, total;
+};
+
+constexpr int kSymGrid = 148;  // persistent CTAs (one per B200 SM): fixed, so results do not depend on the device
+
+int64_t sym_items(int nsb, int k, int nchunks) {
+  const int64_t qq = nsb / k;
+  return (int64_t)nsb * nchunks - ((int64_t)k * qq * (qq - 1) / 2 + qq * (nsb - qq * k));
+}
+
+NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
+  NodePlan p;
+  p.mode = mode;
+  p.N = N;
+  p.Npad = ceil_div(N, kTile) * kTile;  // a multiple of 128: whole 64-node blocks and 128-target blocks
+  p.nb = static_cast<int>(p.Npad / kBlk);
+  p.nsb = static_cast<int>(ceil_div(p.nb, kSymWarps));
+  // R blocks per item: the largest multiple of the warp count (<= 4 of them, SMEM) that still
+  // gives every CTA >= 16 items (balance of the static assignment)
+  int k = 4;
+  for (; k > 1; --k) {
+    const int nch = static_cast<int>(ceil_div(p.nb, k * kSymWarps));
+    if (sym_items(p.nsb, k, nch) >= 16 * kSymGrid) break;
+  }
+  p.chunk = k * kSymWarps;
+  p.nchunks = static_cast<int>(ceil_div(p.nb, p.chunk));
+  p.n_items = sym_items(p.nsb, k, p.nchunks);
+  p.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kSymGrid, p.n_items)));
+  p.sym_smem = (size_t)kSymStages * kBlkTileBytes + (size_t)kSymWarps * 6 * kBlk * 8 + (size_t)6 * p.chunk * kBlk * 8;
+  p.cub_bytes = cub_sort_bytes(N);
+  const int64_t groups = p.Npad / 32;
+  p.near_phases = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));
+  if (phases_override > 0) p.near_phases = std::min(phases_override, 64);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  p.off_box = take(8 * sizeof(double));
+  p.off_skin = take(N * 4);
+  p.off_skout = take(N * 4);
+  p.off_svin = take(N * 4);
+  p.off_svout = take(N * 4);
+  p.off_cub = take(p.cub_bytes);
+  p.off_src = take(p.Npad * kSrcDoubles * sizeof(double));
+  p.off_srcbox = take((p.Npad / kSub + p.Npad / 16) * 8 * sizeof(double));
+  p.off_blkbox = take((size_t)p.nb * 8 * sizeof(double));
+  p.off_nsoa = take(p.Npad * kNodeFields * sizeof(double));
+  p.off_tgt = take(p.Npad * kTgtFields * sizeof(double));
+  p.off_orig = take(p.Npad * sizeof(int32_t));
+  p.off_pacc = take((size_t)p.G * 6 * p.Npad * sizeof(double));
+  p.off_near = take((size_t)p.near_phases * p.Npad * 6 * sizeof(double));
+  p.off_counter = take(sizeof(int) * 8);
+  p.total = off;
+  return p;
+}
+
+template <int MODE>
+int run_nodes(const double* sx, const double* sn, const double* sw, const double* f, const double* q, int64_t N,
+              double h, const double* rho, double* out_u, double* out_v, char* ws, const NodePlan& P, cudaStream_t s,
+              stokes_er_options* opt) {
+  long long* box = reinterpret_cast<long long*>(ws + P.off_box);
+  uint32_t* skin = reinterpret_cast<uint32_t*>(ws + P.off_skin);
+  uint32_t* skout = reinterpret_cast<uint32_t*>(ws + P.off_skout);
+  int32_t* svin = reinterpret_cast<int32_t*>(ws + P.off_svin);
+  int32_t* svout = reinterpret_cast<int32_t*>(ws + P.off_svout);
+  double* src = reinterpret_cast<double*>(ws + P.off_src);
+  double* srcbox = reinterpret_cast<double*>(ws + P.off_srcbox);
+  double* blkbox = reinterpret_cast<double*>(ws + P.off_blkbox);
+  double* nsoa = reinterpret_cast<double*>(ws + P.off_nsoa);
+  double* tgt = reinterpret_cast<double*>(ws + P.off_tgt);
+  int32_t* orig = reinterpret_cast<int32_t*>(ws + P.off_orig);
+  double* pacc = reinterpret_cast<double*>(ws + P.off_pacc);
+  double* near_out = reinterpret_cast<double*>(ws + P.off_near);
+  int* counter = reinterpret_cast<int*>(ws + P.off_counter);
+
+  if (cudaMemsetAsync(box, 0x7f, 3 * sizeof(long long), s) != cudaSuccess ||
+      cudaMemsetAsync(box + 3, 0x80, 3 * sizeof(long long), s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  bbox_kernel<<<static_cast<int>(std::min<int64_t>(2 * 148, ceil_div(N, 256))), 256, 0, s>>>(sx, N, sx, 0, box);
+  morton_kernel<<<ceil_div(N, 256), 256, 0, s>>>(sx, N, box, skin, svin);
+  size_t cb = P.cub_bytes;
+  if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, skin, skout, svin, svout, (int)N, 0, 30, s) !=
+      cudaSuccess)
+    return STOKES_ER_ECUDA;
+  pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox);
+  Delta3 r3{{rho[0], rho[1], rho[2]}};
+  pack_node_soa<MODE><<<ceil_div(P.Npad, 256), 256, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, h, r3, nsoa, tgt,
+                                                             orig);
+  block_boxes<<<ceil_div(P.nb, 256), 256, 0, s>>>(srcbox, P.nb, blkbox);
+  if (cudaMemsetAsync(pacc, 0, (size_t)P.G * 6 * P.Npad * sizeof(double), s) != cudaSuccess ||
+      cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  const double dmax = rho[2] * h;
+  const double rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  SymParams sp;
+  sp.nsoa = nsoa;
+  sp.blk_box = blkbox;
+  sp.pacc = pacc;
+  sp.Npad = P.Npad;
+  sp.nb = P.nb;
+  sp.nsb = P.nsb;
+  sp.chunk = P.chunk;
+  sp.nchunks = P.nchunks;
+  sp.n_items = P.n_items;
+  sp.rc2_box = rc2 * (1.0 + 1e-9);
+  NearParams np;
+  np.src = src;
+  np.src_box = srcbox;
+  np.tgt = tgt;
+  np.near_out = near_out;
+  np.counter = counter + 1;
+  np.phases = P.near_phases;
+  np.n_units = static_cast<int>((P.Npad / 32) * P.near_phases);
+  np.Mpad = P.Npad;
+  np.Npad = P.Npad;
+  np.rc2 = rc2;
+  np.rc2_box = sp.rc2_box;
+  for (int k = 0; k < 3; ++k) np.inv_delta[k] = 1.0 / (rho[k] * h);
+  if (cudaFuncSetAttribute(sym_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.sym_smem) !=
+      cudaSuccess)
+    return STOKES_ER_ECUDA;
+  if (opt && opt->pair_kernel_start_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
+  sym_kernel<MODE><<<P.G, kSymThreads, P.sym_smem, s>>>(sp);
+  if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
+  if (opt && opt->near_kernel_start_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_start_event), s);
+  {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbr_kernel<MODE>, 64, 0);
+    const int ngrid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(ceil_div(np.n_units, 2), (int64_t)sms * std::max(occ, 1))));
+    nbr_kernel<MODE><<<ngrid, 64, 0, s>>>(np, blkbox);
+  }
+  if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
+  if (opt) {
+    opt->stats[0] = P.n_items;
+    opt->stats[1] = P.G;
+    opt->stats[2] = P.chunk;
+    opt->stats[3] = 2;
+  }
+  finalize_nodes<MODE><<<ceil_div(N, 256), 256, 0, s>>>(pacc, P.G, near_out, P.near_phases, tgt, orig, N, P.Npad,
+                                                         out_u, out_v);
+  return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+size_t node_host_stage_bytes(int64_t N) { return align_up(13 * N * sizeof(double)) + align_up(6 * N * sizeof(double)) + 2 * kAlign; }
 
 bool tree_params_ok(const stokes_er_tree_params* tp) {
   return tp && tp->leaf_size >= 1 && tp->degree >= 1 && tp->degree <= kTreeMaxDegree && std::isfinite(tp->theta) &&
@@ -679,6 +841,112 @@ int stokes_er_extrapolate(const double* tgt_b, int64_t M, double h, const double
   extrapolate_kernel<<<ceil_div(M, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tgt_b, M, h, r3, in_delta,
                                                                                        C, out);
   return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+size_t stokes_er_nodes_workspace_bytes(int64_t N, int mode) {
+  if (N < 1 || N > INT32_MAX || mode < 1 || mode > 3) return 0;
+  return make_node_plan(N, mode).total;
+}
+
+size_t stokes_er_nodes_workspace_bytes_ex(int64_t N, int mode, const stokes_er_options* options) {
+  if (N < 1 || N > INT32_MAX || mode < 1 || mode > 3) return 0;
+  return make_node_plan(N, mode, opt_phases(options)).total;
+}
+
+int stokes_er_eval_nodes_ex(const double* src_xyz, const double* src_normal, const double* src_weight,
+                            const double* f, const double* q, int64_t N, double h, const double rho[3], int mode,
+                            double* out_u, double* out_v, void* workspace, size_t workspace_bytes, void* stream,
+                            stokes_er_options* options) {
+  int st = validate(src_xyz, src_normal, src_weight, f, q, src_xyz, src_xyz, src_xyz, N, N, h, rho, mode);
+  if (st) return st;
+  if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
+  if ((st = check_arch())) return st;
+  const NodePlan P = make_node_plan(N, mode, opt_phases(options));
+  if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  switch (mode) {
+    case 1: return run_nodes<1>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
+    case 2: return run_nodes<2>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
+    default: return run_nodes<3>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
+  }
+}
+
+int stokes_er_eval_nodes(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
+                         const double* q, int64_t N, double h, const double rho[3], int mode, double* out_u,
+                         double* out_v, void* workspace, size_t workspace_bytes, void* stream) {
+  return stokes_er_eval_nodes_ex(src_xyz, src_normal, src_weight, f, q, N, h, rho, mode, out_u, out_v, workspace,
+                                 workspace_bytes, stream, nullptr);
+}
+
+size_t stokes_er_nodes_host_workspace_bytes(int64_t N, int mode) {
+  const size_t w = stokes_er_nodes_workspace_bytes(N, mode);
+  return w ? align_up(w) + node_host_stage_bytes(N) : 0;
+}
+
+int stokes_er_eval_nodes_host(const double* sx, const double* sn, const double* sw, const double* f, const double* q,
+                              int64_t N, double h, const double rho[3], int mode, double* out_u, double* out_v,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  int st = validate(sx, sn, sw, f, q, sx, sx, sx, N, N, h, rho, mode);
+  if (st) return st;
+  if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
+  if ((st = check_arch())) return st;
+  const size_t wbytes = align_up(stokes_er_nodes_workspace_bytes(N, mode));
+  if (!workspace || workspace_bytes < wbytes + node_host_stage_bytes(N)) return STOKES_ER_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* stage = static_cast<char*>(workspace) + wbytes;
+  double* dsx = reinterpret_cast<double*>(stage);
+  double *dsn = dsx + 3 * N, *dsw = dsn + 3 * N, *df = dsw + N, *dq = df + 3 * N;
+  double* du = reinterpret_cast<double*>(stage + align_up(13 * N * sizeof(double)));
+  double* dv = du + 3 * N;
+  auto h2d = [&](double* dst, const double* src, int64_t n) {
+    return src ? cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, s) : cudaSuccess;
+  };
+  if (h2d(dsx, sx, 3 * N) || h2d(dsn, sn, 3 * N) || h2d(dsw, sw, N) || h2d(df, (mode & 1) ? f : nullptr, 3 * N) ||
+      h2d(dq, (mode & 2) ? q : nullptr, 3 * N))
+    return STOKES_ER_ECUDA;
+  st = stokes_er_eval_nodes_ex(dsx, dsn, dsw, (mode & 1) ? df : nullptr, (mode & 2) ? dq : nullptr, N, h, rho, mode,
+                               (mode & 1) ? du : nullptr, (mode & 2) ? dv : nullptr, workspace, wbytes, stream,
+                               nullptr);
+  if (st) return st;
+  if ((mode & 1) && cudaMemcpyAsync(out_u, du, 3 * N * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  if ((mode & 2) && cudaMemcpyAsync(out_v, dv, 3 * N * sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  return cudaStreamSynchronize(s) == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
+}
+
+int stokes_er_nodes_pair_counts(int64_t N, int mode, double h, const double rho[3], void* workspace,
+                                size_t workspace_bytes, int64_t* counts_host, void* stream) {
+  if (N < 1 || N > INT32_MAX || mode < 1 || mode > 3 || !(h > 0.0) || !std::isfinite(h) || !rho_ok(rho) ||
+      !counts_host)
+    return STOKES_ER_EINVAL;
+  int st = check_arch();
+  if (st) return st;
+  const NodePlan P = make_node_plan(N, mode);
+  if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(ws + P.off_counter + 2 * sizeof(int) + 8);
+  const double dmax = rho[2] * h;
+  const double rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  if (cudaMemsetAsync(d, 0, sizeof(unsigned long long), s) != cudaSuccess) return STOKES_ER_ECUDA;
+  sym_pair_count<<<ceil_div(P.nb, 128), 128, 0, s>>>(reinterpret_cast<const double*>(ws + P.off_blkbox), P.nb, N,
+                                                     rc2 * (1.0 + 1e-9), d);
+  unsigned long long c = 0;
+  if (cudaMemcpyAsync(&c, d, sizeof(c), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
+  counts_host[0] = static_cast<int64_t>(c);
+  counts_host[1] = N * N - static_cast<int64_t>(c);
+  return STOKES_ER_OK;
+}
+
+int stokes_er_nodes_launch_count(int64_t N, int mode) {
+  (void)mode;
+  // bbox, morton, pack_sources, pack_node_soa, block_boxes, sym_kernel, nbr_kernel, finalize_nodes
+  // (+ the CUB radix sort's own launches, library code)
+  return N > 0 ? 8 : 0;
 }
 
 int stokes_er_launch_count(int64_t M, int64_t N, int mode) {

@@ -1,0 +1,505 @@
+// sym.cuh -- the node-target path (stokes_er_eval_nodes): every quadrature node
+// is also a target (b = 0, x0 = the node, n0 = its normal, f(x0) = f and
+// q(x0) = q at the node).  The pair sum is then symmetric in geometry: the far
+// pair (i <- j) and (j <- i) share d = x_i - x_j, r^2, 1/r and its powers
+// (eqs. (3)-(4): S is even in d, T odd), and for node targets even the
+// stresslet's d.(q_j - q_i) is shared (q0_i = q_i).  One evaluation of the
+// shared part serves both directions.
+//
+// Pipeline (after K0 sort/pack of the general path):
+//   pack_node_soa      node records as SoA 32-node tiles [Npad/32][13][32]
+//                      (x | m w | f w | q | alpha) and the node-target fields
+//   block_boxes        64-node block boxes (union of the two 32-node boxes)
+//   sym_kernel         K5: every unordered pair of 64-node blocks (m < n) whose
+//                      boxes are beyond the cutoff ("AF": all far) -- both
+//                      directions of all 4096 pairs, far-field sums only
+//   nbr_kernel         K6: per 32-target group, every source sub-tile of its own
+//                      block or of a block that is not AF: far pairs (masked)
+//                      and the near 3-delta pairs (the near unit's queue)
+//   finalize_nodes     K7: sums the per-CTA accumulators (fixed order) and the
+//                      K6 partials, applies 1/(8 pi), -6 and chi q0 = q/2
+//
+// Determinism: sym_kernel assigns items to CTAs statically (item i -> CTA
+// i mod G) and every CTA accumulates into its OWN slice of the workspace, in
+// item order; finalize sums the slices in CTA order.  No atomics on data.
+#pragma once
+#include "kernels.cuh"
+
+namespace ser {
+
+constexpr int kNodeFields = 13;  // SoA tile rows: x y z | mx my mz | fx fy fz | qx qy qz | alpha
+enum NodeField { NX = 0, NY, NZ, NMX, NMY, NMZ, NFX, NFY, NFZ, NQX, NQY, NQZ, NALPHA };
+constexpr int kBlk = 64;                                   // nodes per symmetric block (2 sub-tiles)
+constexpr int kBlkTileBytes = 2 * kNodeFields * 32 * 8;    // one R block in SMEM (TMA unit): 6656 B
+#ifndef SER_SYM_WARPS
+#define SER_SYM_WARPS 12
+#endif
+constexpr int kSymWarps = SER_SYM_WARPS;                   // I blocks per CTA (one per warp)
+constexpr int kSymThreads = kSymWarps * 32;
+constexpr int kSymStages = 3;                              // R-block TMA ring
+
+struct SymParams {
+  const double* nsoa;     // [Npad/32][13][32]
+  const double* blk_box;  // [nb][8] lo xyz, pad, hi xyz, pad
+  double* pacc;           // [G][6][Npad] per-CTA accumulators (zeroed by the host)
+  int64_t Npad;
+  int nb;                 // 64-node blocks
+  int nsb;                // superblocks of kSymWarps blocks
+  int chunk;              // R blocks per item (a multiple of kSymWarps)
+  int nchunks;
+  int64_t n_items;
+  double rc2_box;
+};
+
+// Box-level "all far" test between 64-node blocks, symmetric in (a, b): every
+// pair has r^2 >= gap^2 > rc2 (1 + 1e-9).  The same expression decides which
+// pairs sym_kernel owns and which nbr_kernel owns.
+__device__ __forceinline__ bool blocks_far(const double* __restrict__ bb, int a, int b, double rc2_box) {
+  const double* A = bb + (int64_t)a * 8;
+  const double* B = bb + (int64_t)b * 8;
+  double g2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double gap = fmax(0.0, fmax(__ldg(B + d) - __ldg(A + 4 + d), __ldg(A + d) - __ldg(B + 4 + d)));
+    g2 = fma(gap, gap, g2);
+  }
+  return g2 > rc2_box;
+}
+
+// ---------------------------------------------------------------- K0 extras
+// SoA node tiles + node-target fields (y = x, alpha = f.n, q0 = q, n0 = n, b = 0,
+// extrapolation weights at lambda = 0) in Morton order; i >= N are padding
+// copies of the last node with zero weight (they add exactly 0 as sources, and
+// their target sums are dropped).
+template <int MODE>
+__global__ void pack_node_soa(const double* __restrict__ xyz, const double* __restrict__ nrm,
+                              const double* __restrict__ wgt, const double* __restrict__ f,
+                              const double* __restrict__ q, int64_t N, int64_t Npad, const int32_t* __restrict__ perm,
+                              double h, Delta3 rho, double* __restrict__ nsoa, double* __restrict__ tgt,
+                              int32_t* __restrict__ orig) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= Npad) return;
+  const bool pad = i >= N;
+  const int64_t j = perm[pad ? N - 1 : i];
+  const double w = pad ? 0.0 : wgt[j];
+  double x[3], n[3], fv[3], qv[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    x[d] = xyz[d * N + j];
+    n[d] = nrm[d * N + j];
+    fv[d] = (MODE & 1) ? f[d * N + j] : 0.0;
+    qv[d] = (MODE & 2) ? q[d * N + j] : 0.0;
+  }
+  const double alpha = fma(fv[0], n[0], fma(fv[1], n[1], fv[2] * n[2]));  // f(x0).n0
+  double* t = nsoa + (i >> 5) * (kNodeFields * 32) + (i & 31);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    t[(NX + d) * 32] = x[d];
+    t[(NMX + d) * 32] = n[d] * w;
+    t[(NFX + d) * 32] = fv[d] * w;
+    t[(NQX + d) * 32] = qv[d];
+  }
+  t[NALPHA * 32] = alpha;
+  double wk[3];
+  extrap_weights(0.0, h, rho.rho, STOKES_ER_CUTOFF, wk);
+  tgt[F_Y0 * Npad + i] = x[0];
+  tgt[F_Y1 * Npad + i] = x[1];
+  tgt[F_Y2 * Npad + i] = x[2];
+  tgt[F_ALPHA * Npad + i] = alpha;
+  tgt[F_Q0 * Npad + i] = qv[0];
+  tgt[F_Q1 * Npad + i] = qv[1];
+  tgt[F_Q2 * Npad + i] = qv[2];
+  tgt[F_N0 * Npad + i] = n[0];
+  tgt[F_N1 * Npad + i] = n[1];
+  tgt[F_N2 * Npad + i] = n[2];
+  tgt[F_B * Npad + i] = 0.0;
+  tgt[F_W0 * Npad + i] = wk[0];
+  tgt[F_W1 * Npad + i] = wk[1];
+  tgt[F_W2 * Npad + i] = wk[2];
+  orig[i] = static_cast<int32_t>(pad ? -1 : j);
+}
+
+__global__ void block_boxes(const double* __restrict__ box32, int nb, double* __restrict__ bb) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= nb) return;
+  const double* a = box32 + (int64_t)(2 * m) * 8;
+  const double* b = a + 8;
+  double* o = bb + (int64_t)m * 8;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    o[d] = fmin(a[d], b[d]);
+    o[4 + d] = fmax(a[4 + d], b[4 + d]);
+  }
+  o[3] = 0.0;
+  o[7] = 0.0;
+}
+
+// ---------------------------------------------------------------- K5
+struct SymNode {
+  double x, y, z, mx, my, mz, fx, fy, fz, qx, qy, qz, alpha;
+};
+
+template <int MODE>
+__device__ __forceinline__ SymNode load_node(const double* __restrict__ t, int l) {
+  SymNode n;
+  n.x = t[NX * 32 + l]; n.y = t[NY * 32 + l]; n.z = t[NZ * 32 + l];
+  n.mx = t[NMX * 32 + l]; n.my = t[NMY * 32 + l]; n.mz = t[NMZ * 32 + l];
+  if (MODE & 1) {
+    n.fx = t[NFX * 32 + l]; n.fy = t[NFY * 32 + l]; n.fz = t[NFZ * 32 + l];
+    n.alpha = t[NALPHA * 32 + l];
+  } else {
+    n.fx = n.fy = n.fz = n.alpha = 0.0;
+  }
+  if (MODE & 2) {
+    n.qx = t[NQX * 32 + l]; n.qy = t[NQY * 32 + l]; n.qz = t[NQZ * 32 + l];
+  } else {
+    n.qx = n.qy = n.qz = 0.0;
+  }
+  return n;
+}
+
+// Both directions of one far pair (node I, node R), d = x_I - x_R:
+//   u_I += S(d) (f_R w_R - alpha_I m_R w_R),  u_R += S(-d) (f_I w_I - alpha_R m_I w_I)
+//   v_I += T(d) (q_R - q_I) m_R w_R,           v_R += T(-d) (q_I - q_R) m_I w_I
+// with S(d) g = g/r + d (d.g)/r^3 (eq. (3), even in d) and T(d) dq mw =
+// d (d.dq)(d.mw)/r^5 (eq. (4) without the -6, odd in d: the two sign flips of the
+// reverse direction cancel).  61 FP64 instructions for the two directed pairs
+// (41 for one directed pair in far_pair).
+template <int MODE>
+__device__ __forceinline__ void sym_pair(const SymNode& I, const SymNode& R, Acc& ai, Acc& ar) {
+  const double dx = I.x - R.x, dy = I.y - R.y, dz = I.z - R.z;
+  const double ri = rsqrt_nr(fma(dx, dx, fma(dy, dy, dz * dz)));
+  const double ri2 = ri * ri;
+  if (MODE & 1) {
+    const double gx = fma(-I.alpha, R.mx, R.fx), gy = fma(-I.alpha, R.my, R.fy), gz = fma(-I.alpha, R.mz, R.fz);
+    const double a3 = fma(dx, gx, fma(dy, gy, dz * gz)) * ri2;
+    ai.u0 = fma(fma(dx, a3, gx), ri, ai.u0);
+    ai.u1 = fma(fma(dy, a3, gy), ri, ai.u1);
+    ai.u2 = fma(fma(dz, a3, gz), ri, ai.u2);
+    const double hx = fma(-R.alpha, I.mx, I.fx), hy = fma(-R.alpha, I.my, I.fy), hz = fma(-R.alpha, I.mz, I.fz);
+    const double b3 = fma(dx, hx, fma(dy, hy, dz * hz)) * ri2;
+    ar.u0 = fma(fma(dx, b3, hx), ri, ar.u0);
+    ar.u1 = fma(fma(dy, b3, hy), ri, ar.u1);
+    ar.u2 = fma(fma(dz, b3, hz), ri, ar.u2);
+  }
+  if (MODE & 2) {
+    const double qx = R.qx - I.qx, qy = R.qy - I.qy, qz = R.qz - I.qz;
+    const double c = fma(dx, qx, fma(dy, qy, dz * qz)) * (ri2 * ri2 * ri);
+    const double ci = c * fma(dx, R.mx, fma(dy, R.my, dz * R.mz));
+    const double cr = c * fma(dx, I.mx, fma(dy, I.my, dz * I.mz));
+    ai.v0 = fma(dx, ci, ai.v0);
+    ai.v1 = fma(dy, ci, ai.v1);
+    ai.v2 = fma(dz, ci, ai.v2);
+    ar.v0 = fma(dx, cr, ar.v0);
+    ar.v1 = fma(dy, cr, ar.v1);
+    ar.v2 = fma(dz, cr, ar.v2);
+  }
+}
+
+__device__ __forceinline__ void shfl_acc(Acc& a, int src_lane) {
+  a.u0 = __shfl_sync(0xffffffffu, a.u0, src_lane);
+  a.u1 = __shfl_sync(0xffffffffu, a.u1, src_lane);
+  a.u2 = __shfl_sync(0xffffffffu, a.u2, src_lane);
+  a.v0 = __shfl_sync(0xffffffffu, a.v0, src_lane);
+  a.v1 = __shfl_sync(0xffffffffu, a.v1, src_lane);
+  a.v2 = __shfl_sync(0xffffffffu, a.v2, src_lane);
+}
+
+// item -> (superblock s, chunk c): superblock s pairs with chunks c >= s / k
+// (k = chunk / kSymWarps superblocks per chunk); items are numbered s-major.
+__device__ __forceinline__ int64_t items_before(int64_t s, int k, int nchunks) {
+  const int64_t qq = s / k;  // sum_{s' < s} floor(s'/k) = k q(q-1)/2 + q (s - q k)
+  return s * nchunks - (k * qq * (qq - 1) / 2 + qq * (s - qq * k));
+}
+
+// Dynamic SMEM: R-block ring [kSymStages][2][13][32] | red [kSymWarps][6][64] |
+// chunk accumulator [6][chunk * 64].
+template <int MODE>
+__global__ void __launch_bounds__(kSymThreads, 1) sym_kernel(const SymParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);
+  double* red = ring + kSymStages * 2 * kNodeFields * 32;
+  double* cacc = red + kSymWarps * 6 * kBlk;
+  __shared__ __align__(8) uint64_t bar[kSymStages];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int k = p.chunk / kSymWarps;
+  const int cw = p.chunk * kBlk;  // accumulator columns
+  if (tid == 0) {
+    for (int b = 0; b < kSymStages; ++b) mbar_init(&bar[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase_bits = 0;
+  double* my_acc = p.pacc + (int64_t)blockIdx.x * 6 * p.Npad;
+
+  for (int64_t item = blockIdx.x; item < p.n_items; item += G) {
+    // item -> (s, c): binary search on the s-major prefix counts
+    int64_t lo = 0, hi = p.nsb - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (items_before(mid, k, p.nchunks) <= item) lo = mid; else hi = mid - 1;
+    }
+    const int s = static_cast<int>(lo);
+    const int c = static_cast<int>(s / k + (item - items_before(lo, k, p.nchunks)));
+    const int myblk = s * kSymWarps + warp;
+    const int r0 = c * p.chunk;
+    const int nr = min(p.chunk, p.nb - r0);
+    // this item's R blocks that can pair with some warp's I block: n > s W
+    const int n_first = max(r0, s * kSymWarps + 1);
+    const int first = n_first - r0;  // index of the first R block processed
+    const bool has_i = myblk < p.nb;
+
+    // I block of this warp in registers (T = 2 nodes per lane)
+    SymNode I0, I1;
+    Acc a0{0, 0, 0, 0, 0, 0}, a1{0, 0, 0, 0, 0, 0};
+    if (has_i) {
+      const double* t = p.nsoa + (int64_t)(2 * myblk) * kNodeFields * 32;
+      I0 = load_node<MODE>(t, lane);
+      I1 = load_node<MODE>(t + kNodeFields * 32, lane);
+    }
+    for (int x = tid; x < 6 * cw; x += kSymThreads) cacc[x] = 0.0;
+    __syncthreads();  // cacc zeroed; the previous item's readers of the ring are done
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int b = 0; b < kSymStages && first + b < nr; ++b) {
+        mbar_expect_tx(&bar[b], kBlkTileBytes);
+        bulk_g2s(ring + b * 2 * kNodeFields * 32, p.nsoa + (int64_t)(2 * (r0 + first + b)) * kNodeFields * 32,
+                 kBlkTileBytes, &bar[b]);
+      }
+    }
+    for (int ri = first; ri < nr; ++ri) {
+      const int st = (ri - first) % kSymStages;
+      mbar_wait(&bar[st], (phase_bits >> st) & 1u);
+      phase_bits ^= 1u << st;
+      const int n = r0 + ri;
+      const bool active = has_i && n > myblk && blocks_far(p.blk_box, myblk, n, p.rc2_box);
+      const double* R = ring + st * 2 * kNodeFields * 32;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        Acc ra{0, 0, 0, 0, 0, 0};
+        if (active) {
+          const double* Rt = R + hf * kNodeFields * 32;
+#pragma unroll 2
+          for (int kk = 0; kk < 32; ++kk) {
+            const SymNode rn = load_node<MODE>(Rt, (lane + kk) & 31);
+            sym_pair<MODE>(I0, rn, a0, ra);
+            sym_pair<MODE>(I1, rn, a1, ra);
+            shfl_acc(ra, (lane + 1) & 31);  // lane l holds node (l + kk + 1) & 31 next
+          }
+        }
+        // lane l holds R node hf * 32 + l
+        double* rw = red + warp * 6 * kBlk + hf * 32 + lane;
+        rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
+        rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
+      }
+      __syncthreads();  // red complete; every warp is done reading ring[st]
+      if (tid == 0 && ri + kSymStages < nr) {  // refill the stage just released
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[st], kBlkTileBytes);
+        bulk_g2s(ring + st * 2 * kNodeFields * 32, p.nsoa + (int64_t)(2 * (n + kSymStages)) * kNodeFields * 32,
+                 kBlkTileBytes, &bar[st]);
+      }
+      for (int x = tid; x < 6 * kBlk; x += kSymThreads) {  // fixed warp order: deterministic
+        const int comp = x / kBlk, col = x - comp * kBlk;
+        double sum = 0.0;
+#pragma unroll 4
+        for (int w = 0; w < kSymWarps; ++w) sum += red[(w * 6 + comp) * kBlk + col];
+        cacc[comp * cw + ri * kBlk + col] += sum;
+      }
+      __syncthreads();  // red may be overwritten
+    }
+    // flush: I sums of every warp, then the chunk's R sums (both into this CTA's slice, in order)
+    if (has_i) {
+      const int64_t i0 = (int64_t)myblk * kBlk + lane, i1 = i0 + 32;
+      double* a = my_acc;
+      a[0 * p.Npad + i0] += a0.u0; a[1 * p.Npad + i0] += a0.u1; a[2 * p.Npad + i0] += a0.u2;
+      a[3 * p.Npad + i0] += a0.v0; a[4 * p.Npad + i0] += a0.v1; a[5 * p.Npad + i0] += a0.v2;
+      a[0 * p.Npad + i1] += a1.u0; a[1 * p.Npad + i1] += a1.u1; a[2 * p.Npad + i1] += a1.u2;
+      a[3 * p.Npad + i1] += a1.v0; a[4 * p.Npad + i1] += a1.v1; a[5 * p.Npad + i1] += a1.v2;
+    }
+    __syncthreads();  // I flush before the R flush (a diagonal chunk holds the same nodes)
+    for (int x = tid; x < 6 * nr * kBlk; x += kSymThreads) {
+      const int comp = x / (nr * kBlk), col = x - comp * (nr * kBlk);
+      my_acc[comp * p.Npad + (int64_t)r0 * kBlk + col] += cacc[comp * cw + col];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K6
+// Neighbour unit: 32 Morton-consecutive node targets (lane = target) x every
+// source sub-tile of their own 64-node block or of a block that is not AF with
+// it (blocks_far false): exactly the directed pairs sym_kernel does not own.
+// Far pairs of those sub-tiles (r^2 > rc2) are summed here with the near pairs
+// masked (far_pair_masked); near pairs go through the near unit's per-lane queue
+// and near_pair (3 deltas, weights folded).  One unit = (group, phase), phase p
+// takes every phases-th selected sub-tile.
+struct NbrSmem {
+  double src[kSrcDoubles][32];
+  int q[kQCap][32];
+  double tf[kNearFields][32];
+};
+
+template <int MODE>
+__device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __restrict__ blk_box, int unit,
+                                         NbrSmem& sm) {
+  const int lane = threadIdx.x & 31;
+  int(*q)[32] = sm.q;
+  double(*tf)[32] = sm.tf;
+  const int n_sub = static_cast<int>(p.Npad / kSub);
+  const int64_t g = unit / p.phases;
+  const int phase = unit - static_cast<int>(g) * p.phases;
+  const int tblk = static_cast<int>(g >> 1);
+  const int64_t ti = g * 32 + lane;
+  Tgt tg;
+  tg.y0 = p.tgt[F_Y0 * p.Mpad + ti];
+  tg.y1 = p.tgt[F_Y1 * p.Mpad + ti];
+  tg.y2 = p.tgt[F_Y2 * p.Mpad + ti];
+  tg.alpha = (MODE & 1) ? p.tgt[F_ALPHA * p.Mpad + ti] : 0.0;
+  tg.q0 = (MODE & 2) ? p.tgt[F_Q0 * p.Mpad + ti] : 0.0;
+  tg.q1 = (MODE & 2) ? p.tgt[F_Q1 * p.Mpad + ti] : 0.0;
+  tg.q2 = (MODE & 2) ? p.tgt[F_Q2 * p.Mpad + ti] : 0.0;
+  __syncwarp();
+  {
+    const double* tq = p.tgt + ti;
+    tf[NF_ALPHA][lane] = tg.alpha;
+    tf[NF_Q0][lane] = tg.q0;
+    tf[NF_Q1][lane] = tg.q1;
+    tf[NF_Q2][lane] = tg.q2;
+    tf[NF_N0][lane] = tq[F_N0 * p.Mpad];
+    tf[NF_N1][lane] = tq[F_N1 * p.Mpad];
+    tf[NF_N2][lane] = tq[F_N2 * p.Mpad];
+    tf[NF_B][lane] = tq[F_B * p.Mpad];
+    tf[NF_W0][lane] = tq[F_W0 * p.Mpad];
+    tf[NF_W1][lane] = tq[F_W1 * p.Mpad];
+    tf[NF_W2][lane] = tq[F_W2 * p.Mpad];
+  }
+  Acc fa{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  NearAcc acc{0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int head = 0, tail = 0, ordinal = 0, base = 0;
+  unsigned mm = 0;
+  for (;;) {
+    while (mm == 0 && base < n_sub) {
+      const int sb = base + lane;
+      const bool sel = sb < n_sub && ((sb >> 1) == tblk || !blocks_far(blk_box, tblk, sb >> 1, p.rc2_box));
+      mm = __ballot_sync(0xffffffffu, sel);
+      unsigned keep = 0, m = mm;
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (ordinal % p.phases == phase) keep |= 1u << bit;
+        ++ordinal;
+      }
+      mm = keep;
+      base += 32;
+    }
+    int rounds;
+    const bool last = (mm == 0);
+    if (!last) {
+      const int sub = base - 32 + __ffs(mm) - 1;
+      mm &= mm - 1;
+      {
+        const double* gs = p.src + ((int64_t)sub * kSub + lane) * kSrcDoubles;
+#pragma unroll
+        for (int f = 0; f < kSrcDoubles; ++f) sm.src[f][lane] = __ldg(gs + f);
+      }
+      __syncwarp();
+      unsigned smask = 0;
+#pragma unroll 2
+      for (int kk = 0; kk < 32; ++kk) {
+        Src s;
+        s.x = sm.src[0][kk]; s.y = sm.src[1][kk]; s.z = sm.src[2][kk];
+        s.mx = sm.src[3][kk]; s.my = sm.src[4][kk]; s.mz = sm.src[5][kk];
+        s.fx = sm.src[6][kk]; s.fy = sm.src[7][kk]; s.fz = sm.src[8][kk];
+        s.qx = sm.src[9][kk]; s.qy = sm.src[10][kk]; s.qz = sm.src[11][kk];
+        const double dx = tg.y0 - s.x, dy = tg.y1 - s.y, dz = tg.y2 - s.z;
+        const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+        smask |= (r2 <= p.rc2 ? 1u : 0u) << kk;
+        far_pair_masked<MODE>(s, tg, fa, p.rc2);
+      }
+      __syncwarp();
+      while (smask) {
+        const int bit = __ffs(smask) - 1;
+        smask &= smask - 1;
+        q[tail & (kQCap - 1)][lane] = sub * kSub + bit;
+        ++tail;
+      }
+      const int minlen = __reduce_min_sync(0xffffffffu, tail - head);
+      const int maxlen = __reduce_max_sync(0xffffffffu, tail - head);
+      rounds = max(minlen >= 32 ? minlen : 0, maxlen - (kQCap - 32));
+    } else {
+      rounds = __reduce_max_sync(0xffffffffu, tail - head);
+    }
+    for (int r = 0; r < rounds; ++r) {
+      if (head < tail) {
+        const int sidx = q[head & (kQCap - 1)][lane];
+        ++head;
+        const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
+        near_pair<MODE, false>(s, tg.y0, tg.y1, tg.y2, tf, lane, p, acc);
+      }
+    }
+    if (last) break;
+  }
+  const double v0 = fma(-tf[NF_N0][lane], acc.kn, acc.v0), v1 = fma(-tf[NF_N1][lane], acc.kn, acc.v1),
+               v2 = fma(-tf[NF_N2][lane], acc.kn, acc.v2);
+  __syncwarp();
+  double* out = p.near_out + (int64_t)phase * 6 * p.Mpad + ti;
+  out[0 * p.Mpad] = fa.u0 + acc.u0; out[1 * p.Mpad] = fa.u1 + acc.u1; out[2 * p.Mpad] = fa.u2 + acc.u2;
+  out[3 * p.Mpad] = fa.v0 + v0; out[4 * p.Mpad] = fa.v1 + v1; out[5 * p.Mpad] = fa.v2 + v2;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(64, 6) nbr_kernel(const NearParams p, const double* __restrict__ blk_box) {
+  __shared__ NbrSmem s_nb[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    int unit = 0;
+    if (lane == 0) unit = atomicAdd(p.counter, 1);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= p.n_units) break;
+    nbr_unit<MODE>(p, blk_box, unit, s_nb[warp]);
+  }
+}
+
+// Statistics (not on the hot path): directed pairs of real nodes owned by sym_kernel,
+// 2 n_m n_n over the all-far block pairs m < n (n_m = real nodes of block m).
+__global__ void sym_pair_count(const double* __restrict__ blk_box, int nb, int64_t N, double rc2_box,
+                               unsigned long long* __restrict__ out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= nb) return;
+  const int64_t nm = min((int64_t)kBlk, max((int64_t)0, N - (int64_t)m * kBlk));
+  unsigned long long c = 0;
+  for (int n = m + 1; n < nb; ++n) {
+    const int64_t nn = min((int64_t)kBlk, max((int64_t)0, N - (int64_t)n * kBlk));
+    if (nn > 0 && blocks_far(blk_box, m, n, rc2_box)) c += 2ull * (unsigned long long)(nm * nn);
+  }
+  if (c) atomicAdd(out, c);
+}
+
+// ---------------------------------------------------------------- K7
+template <int MODE>
+__global__ void finalize_nodes(const double* __restrict__ pacc, int G, const double* __restrict__ near_out,
+                               int phases, const double* __restrict__ tgt, const int32_t* __restrict__ orig,
+                               int64_t N, int64_t Npad, double* __restrict__ out_u, double* __restrict__ out_v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  for (int c = 0; c < G; ++c)  // fixed CTA order: deterministic
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if ((k < 3 && (MODE & 1)) || (k >= 3 && (MODE & 2))) s[k] += pacc[((int64_t)c * 6 + k) * Npad + i];
+  for (int ph = 0; ph < phases; ++ph)
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if ((k < 3 && (MODE & 1)) || (k >= 3 && (MODE & 2))) s[k] += near_out[((int64_t)ph * 6 + k) * Npad + i];
+  const int64_t o = orig[i];
+  const double inv8pi = 1.0 / (8.0 * kPi);
+  if (MODE & 1)
+    for (int k = 0; k < 3; ++k) out_u[k * N + o] = s[k] * inv8pi;                            // eq. (10)
+  if (MODE & 2)
+    for (int k = 0; k < 3; ++k)                                                               // eq. (11), chi = 1/2
+      out_v[k * N + o] = -6.0 * s[3 + k] * inv8pi + 0.5 * tgt[(F_Q0 + k) * Npad + i];
+}
+
+}  // namespace ser

@@ -281,7 +281,8 @@ struct TreeFarParams {
   int* counter;
   int64_t Mpad;
   int n_groups, p;
-  double theta, rc2;      // MAC parameter, guard (c delta_max)^2 (1 + 1e-9)
+  double theta, rc2;      // MAC parameter, (c delta_max)^2: the per-pair near rule of the direct sums
+  double rc2_guard;       // R23 acceptance guard: rc2 (1 + 1e-9), the margin of the direct path's box tests
 };
 
 struct __align__(16) TreeWarpSmem {
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(kTreeWarps * 32, SER_TREE_MINB) tree_far_kerne
           if (gap < 0.0) gap = 0.0;
           g2 = __dadd_rn(g2, __dmul_rn(gap, gap));
         }
-        acc_lane = (nd.rc <= __dmul_rn(p.theta, __dsqrt_rn(R2))) && (g2 > p.rc2);
+        acc_lane = (nd.rc <= __dmul_rn(p.theta, __dsqrt_rn(R2))) && (g2 > p.rc2_guard);
       }
       const unsigned accm = __ballot_sync(0xffffffffu, acc_lane);
       // R26: an accepted cluster with at most (p+1)^3 points is summed directly

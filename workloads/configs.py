@@ -188,6 +188,16 @@ def config5(inv_h: int = 128, seed: int = 5, rho=RHO_CONFIGS) -> Block:
                       name=f"cfg5_sphere_h1/{inv_h}", src=(x, n, w), meta={"config": 5, "seed": seed})
 
 
+def node_block(block: Block, name_suffix: str = "_nodes") -> Block:
+    """The Block whose targets are `block`'s own quadrature nodes: y = x, b = 0, x0 = x,
+    n0 = n, f(x0) = f and q(x0) = q at the node -- the argument set of stokes_er_eval that
+    stokes_er_eval_nodes computes (include/stokes_er.h)."""
+    x = block.src_xyz
+    dens = np.concatenate([block.src_normal, block.f, block.q], axis=0)
+    return replace(block, tgt_xyz=_c(x), tgt_b=np.zeros(x.shape[1]), tgt_x0_density=_c(dens), tgt_x0=_c(x),
+                   name=block.name + name_suffix, meta=dict(block.meta, targets="nodes"))
+
+
 def pure_far(inv_h: int = 128, seed: int = 6, b: float = 0.5, rho=RHO_CONFIGS) -> Block:
     """Far-only micro-workload: sphere nodes as sources, M = N targets at b = 0.5.
     Every pair has r >= 0.5 > 6*delta_max for 1/h >= 64."""
