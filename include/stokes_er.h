@@ -226,6 +226,14 @@ int stokes_er_eval_nodes_ex(const double* src_xyz, const double* src_normal, con
                             const double* f, const double* q, int64_t N, double h, const double rho[3], int mode,
                             double* out_u, double* out_v, void* workspace, size_t workspace_bytes, void* stream,
                             stokes_er_options* options);
+/* NEXT-1 at the nodes: stokes_er_eval_onsurface (s# factors of PAPER.md:126-139, one delta,
+ * cutoff STOKES_ER_CUTOFF_SURFACE, no extrapolation) with the targets = the N nodes, through
+ * the same symmetric far kernel.  Workspace: stokes_er_nodes_workspace_bytes(N, mode).  The
+ * two-drop solver's self blocks are exactly this call. */
+int stokes_er_eval_nodes_onsurface(const double* src_xyz, const double* src_normal, const double* src_weight,
+                                   const double* f, const double* q, int64_t N, double delta, int mode,
+                                   double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
+                                   void* stream);
 /* HOST buffers (pinned recommended): H2D, evaluation, D2H, then synchronizes `stream`.
  * Workspace: stokes_er_nodes_host_workspace_bytes(N, mode) device bytes. */
 size_t stokes_er_nodes_host_workspace_bytes(int64_t N, int mode);

@@ -240,6 +240,29 @@ def evaluate_nodes(src_xyz, src_normal, src_weight, f, q, h, rho, mode=BOTH, out
     return (out_u if mode & SL else None), (out_v if mode & DL else None)
 
 
+def evaluate_nodes_onsurface(src_xyz, src_normal, src_weight, f, q, delta, mode=BOTH, out_u=None, out_v=None,
+                             workspace=None, stream=None):
+    """stokes_er_eval_nodes_onsurface: NEXT-1's s# evaluation (one delta, cutoff 7) at the nodes."""
+    N = int(src_xyz.shape[1])
+    for name, t, shp in (("src_xyz", src_xyz, (3, N)), ("src_normal", src_normal, (3, N)),
+                         ("src_weight", src_weight, (N,)), ("f", f if mode & SL else None, (3, N)),
+                         ("q", q if mode & DL else None, (3, N)), ("out_u", out_u if mode & SL else None, (3, N)),
+                         ("out_v", out_v if mode & DL else None, (3, N))):
+        _check_dev(name, t, shp)
+    dev = src_xyz.device
+    if mode & SL and out_u is None:
+        out_u = _out((3, N), dev, stream)
+    if mode & DL and out_v is None:
+        out_v = _out((3, N), dev, stream)
+    if workspace is None:
+        workspace = _scratch(nodes_workspace_bytes(N, mode), dev, stream)
+    _lib.check("stokes_er_eval_nodes_onsurface", _lib.load().stokes_er_eval_nodes_onsurface(
+        _ptr(src_xyz), _ptr(src_normal), _ptr(src_weight), _ptr(f if mode & SL else None),
+        _ptr(q if mode & DL else None), N, float(delta), int(mode), _ptr(out_u if mode & SL else None),
+        _ptr(out_v if mode & DL else None), _ptr(workspace), int(workspace.numel()), _stream_handle(stream)))
+    return (out_u if mode & SL else None), (out_v if mode & DL else None)
+
+
 def nodes_pair_counts(N: int, h, rho, workspace, mode: int = BOTH, stream=None):
     """(directed pairs summed by the symmetric far kernel, pairs owned by the neighbour kernel)
     of the last evaluate_nodes with this workspace (synchronizes; statistics only)."""

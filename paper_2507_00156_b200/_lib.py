@@ -58,7 +58,7 @@ EXPORTS = ["stokes_er_workspace_bytes", "stokes_er_workspace_bytes_ex", "stokes_
            "stokes_er_eval_tree", "stokes_er_eval_tree_onsurface", "stokes_er_nodes_workspace_bytes",
            "stokes_er_nodes_workspace_bytes_ex", "stokes_er_eval_nodes", "stokes_er_eval_nodes_ex",
            "stokes_er_nodes_host_workspace_bytes", "stokes_er_eval_nodes_host", "stokes_er_nodes_launch_count",
-           "stokes_er_nodes_pair_counts"]
+           "stokes_er_nodes_pair_counts", "stokes_er_eval_nodes_onsurface"]
 
 _lib = None
 
@@ -144,6 +144,9 @@ def load():
     L.stokes_er_eval_nodes_host.restype = ctypes.c_int
     L.stokes_er_nodes_launch_count.argtypes = [_i64, ctypes.c_int]
     L.stokes_er_nodes_launch_count.restype = ctypes.c_int
+    L.stokes_er_eval_nodes_onsurface.argtypes = [_dp] * 5 + [_i64, ctypes.c_double, ctypes.c_int, _dp, _dp, _dp,
+                                                 ctypes.c_size_t, _dp]
+    L.stokes_er_eval_nodes_onsurface.restype = ctypes.c_int
     L.stokes_er_nodes_pair_counts.argtypes = [_i64, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double), _dp,
                                               ctypes.c_size_t, ctypes.POINTER(_i64), _dp]
     L.stokes_er_nodes_pair_counts.restype = ctypes.c_int

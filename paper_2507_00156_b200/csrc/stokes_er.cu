@@ -571,7 +571,9 @@ NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
   return p;
 }
 
-template <int MODE>
+// SHARP: NEXT-1's on-surface s# evaluation (h = delta, rho = (1,1,1), cutoff STOKES_ER_CUTOFF_SURFACE,
+// weights (1,0,0)); otherwise the 3-delta extrapolated method.  The far pairs are the same either way.
+template <int MODE, bool SHARP>
 int run_nodes(const double* sx, const double* sn, const double* sw, const double* f, const double* q, int64_t N,
               double h, const double* rho, double* out_u, double* out_v, char* ws, const NodePlan& P, cudaStream_t s,
               stokes_er_options* opt) {
@@ -601,14 +603,15 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
     return STOKES_ER_ECUDA;
   pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox);
   Delta3 r3{{rho[0], rho[1], rho[2]}};
-  pack_node_soa<MODE><<<ceil_div(P.Npad, 256), 256, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, h, r3, nsoa, tgt,
-                                                             orig);
+  pack_node_soa<MODE><<<ceil_div(P.Npad, 256), 256, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, h, r3, SHARP, nsoa,
+                                                             tgt, orig);
   block_boxes<<<ceil_div(P.nb, 256), 256, 0, s>>>(srcbox, P.nb, blkbox);
   if (cudaMemsetAsync(pacc, 0, (size_t)P.G * 6 * P.Npad * sizeof(double), s) != cudaSuccess ||
       cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess)
     return STOKES_ER_ECUDA;
   const double dmax = rho[2] * h;
-  const double rc2 = (STOKES_ER_CUTOFF * dmax) * (STOKES_ER_CUTOFF * dmax);
+  const double cutoff = SHARP ? STOKES_ER_CUTOFF_SURFACE : STOKES_ER_CUTOFF;
+  const double rc2 = (cutoff * dmax) * (cutoff * dmax);
   SymParams sp;
   sp.nsoa = nsoa;
   sp.blk_box = blkbox;
@@ -644,10 +647,10 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbr_kernel<MODE>, 64, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbr_kernel<MODE, SHARP>, 64, 0);
     const int ngrid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(np.n_units, 2), (int64_t)sms * std::max(occ, 1))));
-    nbr_kernel<MODE><<<ngrid, 64, 0, s>>>(np, blkbox);
+    nbr_kernel<MODE, SHARP><<<ngrid, 64, 0, s>>>(np, blkbox);
   }
   if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
   if (opt) {
@@ -866,9 +869,28 @@ int stokes_er_eval_nodes_ex(const double* src_xyz, const double* src_normal, con
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(workspace);
   switch (mode) {
-    case 1: return run_nodes<1>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
-    case 2: return run_nodes<2>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
-    default: return run_nodes<3>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
+    case 1: return run_nodes<1, false>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
+    case 2: return run_nodes<2, false>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
+    default: return run_nodes<3, false>(src_xyz, src_normal, src_weight, f, q, N, h, rho, out_u, out_v, ws, P, s, options);
+  }
+}
+
+int stokes_er_eval_nodes_onsurface(const double* src_xyz, const double* src_normal, const double* src_weight,
+                                   const double* f, const double* q, int64_t N, double delta, int mode, double* out_u,
+                                   double* out_v, void* workspace, size_t workspace_bytes, void* stream) {
+  const double one[3] = {1.0, 1.0, 1.0};  // delta_1 = delta_2 = delta_3 = delta; weights (1, 0, 0)
+  int st = validate(src_xyz, src_normal, src_weight, f, q, src_xyz, src_xyz, src_xyz, N, N, delta, one, mode, false);
+  if (st) return st;
+  if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
+  if ((st = check_arch())) return st;
+  const NodePlan P = make_node_plan(N, mode);
+  if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  switch (mode) {
+    case 1: return run_nodes<1, true>(src_xyz, src_normal, src_weight, f, q, N, delta, one, out_u, out_v, ws, P, s, nullptr);
+    case 2: return run_nodes<2, true>(src_xyz, src_normal, src_weight, f, q, N, delta, one, out_u, out_v, ws, P, s, nullptr);
+    default: return run_nodes<3, true>(src_xyz, src_normal, src_weight, f, q, N, delta, one, out_u, out_v, ws, P, s, nullptr);
   }
 }
 

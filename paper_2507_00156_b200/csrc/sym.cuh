@@ -75,8 +75,8 @@ template <int MODE>
 __global__ void pack_node_soa(const double* __restrict__ xyz, const double* __restrict__ nrm,
                               const double* __restrict__ wgt, const double* __restrict__ f,
                               const double* __restrict__ q, int64_t N, int64_t Npad, const int32_t* __restrict__ perm,
-                              double h, Delta3 rho, double* __restrict__ nsoa, double* __restrict__ tgt,
-                              int32_t* __restrict__ orig) {
+                              double h, Delta3 rho, bool sharp, double* __restrict__ nsoa,
+                              double* __restrict__ tgt, int32_t* __restrict__ orig) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= Npad) return;
   const bool pad = i >= N;
@@ -100,8 +100,8 @@ __global__ void pack_node_soa(const double* __restrict__ xyz, const double* __re
     t[(NQX + d) * 32] = qv[d];
   }
   t[NALPHA * 32] = alpha;
-  double wk[3];
-  extrap_weights(0.0, h, rho.rho, STOKES_ER_CUTOFF, wk);
+  double wk[3] = {1.0, 0.0, 0.0};  // NEXT-1 (s#): one delta, no extrapolation
+  if (!sharp) extrap_weights(0.0, h, rho.rho, STOKES_ER_CUTOFF, wk);
   tgt[F_Y0 * Npad + i] = x[0];
   tgt[F_Y1 * Npad + i] = x[1];
   tgt[F_Y2 * Npad + i] = x[2];
@@ -341,7 +341,7 @@ struct NbrSmem {
   double tf[kNearFields][32];
 };
 
-template <int MODE>
+template <int MODE, bool SHARP>
 __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __restrict__ blk_box, int unit,
                                          NbrSmem& sm) {
   const int lane = threadIdx.x & 31;
@@ -436,7 +436,7 @@ __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __re
         const int sidx = q[head & (kQCap - 1)][lane];
         ++head;
         const Src s = load_src_global<MODE>(p.src + (int64_t)sidx * kSrcDoubles);
-        near_pair<MODE, false>(s, tg.y0, tg.y1, tg.y2, tf, lane, p, acc);
+        near_pair<MODE, SHARP>(s, tg.y0, tg.y1, tg.y2, tf, lane, p, acc);
       }
     }
     if (last) break;
@@ -449,7 +449,7 @@ __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __re
   out[3 * p.Mpad] = fa.v0 + v0; out[4 * p.Mpad] = fa.v1 + v1; out[5 * p.Mpad] = fa.v2 + v2;
 }
 
-template <int MODE>
+template <int MODE, bool SHARP>
 __global__ void __launch_bounds__(64, 6) nbr_kernel(const NearParams p, const double* __restrict__ blk_box) {
   __shared__ NbrSmem s_nb[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(64, 6) nbr_kernel(const NearParams p, const do
     if (lane == 0) unit = atomicAdd(p.counter, 1);
     unit = __shfl_sync(0xffffffffu, unit, 0);
     if (unit >= p.n_units) break;
-    nbr_unit<MODE>(p, blk_box, unit, s_nb[warp]);
+    nbr_unit<MODE, SHARP>(p, blk_box, unit, s_nb[warp]);
   }
 }
 

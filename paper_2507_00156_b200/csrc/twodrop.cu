@@ -187,6 +187,22 @@ __global__ void dot_final_kernel(const double* __restrict__ partial, int nb, dou
   if (threadIdx.x == 0) *out = s;
 }
 
+// MGS update with the coefficient read on the device (no host round trip per dot):
+// w = 1.0 * w + (-h) * v, the same arithmetic as lincomb_kernel(n, 1.0, w, -h, v).
+__global__ void mgs_update_kernel(int64_t n, const double* __restrict__ h, double* w, const double* __restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  w[i] = fma(-*h, v[i], 1.0 * w[i]);
+}
+// *h = ||w||^2 (left in place; the host takes its sqrt after the copy): v = (1/||w||) w when
+// ||w|| > 0, the arithmetic of lincomb_kernel(n, 1.0 / ||w||, w).
+__global__ void mgs_normalize_kernel(int64_t n, const double* __restrict__ h, const double* __restrict__ w,
+                                     double* __restrict__ v) {
+  const double nw = sqrt(*h);
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (nw > 0.0 && i < n) v[i] = (1.0 / nw) * w[i];
+}
+
 // ----------------------------------------------------------------- host side
 size_t al(size_t x) { return (x + 255) / 256 * 256; }
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -196,7 +212,7 @@ struct Layout {
   int max_iter = 0;
   size_t eval_ws = 0;
   size_t off_eval, off_x0s[2], off_x0c[2], off_zero[2], off_vs[2], off_vc[2], off_cnt[2], off_idx[2], off_L[2];
-  size_t off_V, off_w, off_partial, off_scalar, off_status, total;
+  size_t off_V, off_w, off_partial, off_scalar, off_hcol, off_status, total;
 };
 
 Layout layout(int64_t N1, int64_t N2, int max_iter, const stokes_er_twodrop_params* P = nullptr) {
@@ -208,6 +224,7 @@ Layout layout(int64_t N1, int64_t N2, int max_iter, const stokes_er_twodrop_para
   for (int b = 0; b < 2; ++b)
     for (int m = 0; m < 2; ++m) {
       L.eval_ws = std::max(L.eval_ws, stokes_er_workspace_bytes(L.N[b], L.N[m], 3));
+      if (b == m) L.eval_ws = std::max(L.eval_ws, stokes_er_nodes_workspace_bytes(L.N[b], 3));  // self blocks
       if (P && P->use_tree)  // block (targets b <- sources m) through the treecode over drop m
         L.eval_ws = std::max(L.eval_ws, stokes_er_tree_workspace_bytes(L.N[b], L.N[m], 3, P->tree, P->tree_plan[m]));
     }
@@ -233,6 +250,7 @@ Layout layout(int64_t N1, int64_t N2, int max_iter, const stokes_er_twodrop_para
   L.off_w = take(L.n * sizeof(double));
   L.off_partial = take(kDotBlocks * sizeof(double));
   L.off_scalar = take(8 * sizeof(double));
+  L.off_hcol = take((size_t)(max_iter + 2) * sizeof(double));
   L.off_status = take(4 * sizeof(int));
   L.total = off;
   return L;
@@ -307,10 +325,10 @@ int blocks(const Ctx& c, int mode, const double* u, double* out) {
                                          sl ? nullptr : ub, d[b].xyz, c.at<double>(c.L.off_zero[b]), x0s, Nb, Nb,
                                          c.P->delta_self, mode, c.P->tree, c.P->tree_plan[b], sl ? vs : nullptr,
                                          sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
-    else
-      st = stokes_er_eval_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr, sl ? nullptr : ub,
-                                    d[b].xyz, c.at<double>(c.L.off_zero[b]), x0s, Nb, Nb, c.P->delta_self, mode,
-                                    sl ? vs : nullptr, sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
+    else  // the self block's targets are the drop's own nodes: the symmetric node path (same sums)
+      st = stokes_er_eval_nodes_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr,
+                                          sl ? nullptr : ub, Nb, c.P->delta_self, mode, sl ? vs : nullptr,
+                                          sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
     if (st) break;
     if (c.P->use_tree)
       st = stokes_er_eval_tree(d[m].xyz, d[m].normal, d[m].weight, sl ? d[m].f : nullptr, sl ? nullptr : um,
@@ -466,14 +484,24 @@ int stokes_er_twodrop_solve(const stokes_er_drop drops[2], const stokes_er_cross
   for (; j < K; ++j) {
     if ((st = blocks(c, STOKES_ER_DL, Vj(j), w))) return st;
     double* hj = &H[(size_t)j * (K + 1)];
-    for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
-      if ((st = dot(c, w, Vj(i), &hj[i]))) return st;
-      lincomb(c, 1.0, w, -hj[i], Vj(i), w);
+    // modified Gram-Schmidt with the coefficients kept on the device: h_ij = <w, v_i> then
+    // w -= h_ij v_i, in order; ||w|| and v_{j+1}; ONE device->host copy of the column and one
+    // stream synchronization per Krylov step (the Givens update and the stopping test are on
+    // the host).  Same arithmetic as the per-dot host round trip it replaces.
+    double* hcol = c.at<double>(c.L.off_hcol);
+    double* part = c.at<double>(c.L.off_partial);
+    for (int i = 0; i <= j; ++i) {
+      dot_partial_kernel<<<kDotBlocks, 256, 0, c.s>>>(w, Vj(i), n, part);
+      dot_final_kernel<<<1, 32, 0, c.s>>>(part, kDotBlocks, hcol + i);
+      mgs_update_kernel<<<cdiv(n, 256), 256, 0, c.s>>>(n, hcol + i, w, Vj(i));
     }
-    double nw2 = 0.0;
-    if ((st = dot(c, w, w, &nw2))) return st;
+    dot_partial_kernel<<<kDotBlocks, 256, 0, c.s>>>(w, w, n, part);
+    dot_final_kernel<<<1, 32, 0, c.s>>>(part, kDotBlocks, hcol + j + 1);
+    mgs_normalize_kernel<<<cdiv(n, 256), 256, 0, c.s>>>(n, hcol + j + 1, w, Vj(j + 1));
+    if ((st = ok(cudaMemcpyAsync(hj, hcol, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.s)))) return st;
+    if ((st = ok(cudaStreamSynchronize(c.s)))) return st;
+    const double nw2 = hj[j + 1];
     hj[j + 1] = std::sqrt(nw2);
-    if (hj[j + 1] > 0.0) lincomb(c, 1.0 / hj[j + 1], w, 0.0, nullptr, Vj(j + 1));
     for (int i = 0; i < j; ++i) {  // apply the previous rotations to column j
       const double a = hj[i], b2 = hj[i + 1];
       hj[i] = cs[i] * a + sn[i] * b2;

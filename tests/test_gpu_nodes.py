@@ -224,3 +224,29 @@ def test_cuda_graph_capture_and_replay(ser):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out_u, ref[0]) and torch.equal(out_v, ref[1])
+
+
+@pytest.mark.parametrize("inv_h,mode", [(16, 3), (32, 3), (32, 2), (16, 1)])
+def test_onsurface_sharp_at_nodes(ser, inv_h, mode):
+    """NEXT-1 at the nodes (stokes_er_eval_nodes_onsurface: s#, delta = 3h, cutoff 7 --
+    the two-drop self block) against the oracle's sharp mode with node targets (definition:
+    every pair regularized), and against the general stokes_er_eval_onsurface."""
+    import torch
+
+    blk = config5(inv_h=inv_h)
+    delta = 3 * blk.h
+    arrs = [torch.from_numpy(a).cuda() for a in (blk.src_xyz, blk.src_normal, blk.src_weight, blk.f, blk.q)]
+    u, v = ser.evaluate_nodes_onsurface(*arrs, delta, mode=mode)
+    idx = None if inv_h == 16 else sample(blk.N, 300)
+    nb = node_block(blk) if idx is None else node_block(blk).take_targets(idx)
+    ur, vr = oracle.evaluate_sharp(*nb.arrays(), delta, mode=mode, localized=False, cutoff=7.0)
+    pick = (lambda a: a.cpu().numpy()) if idx is None else (lambda a: a.cpu().numpy()[:, idx])
+    if mode & 1:
+        assert rel(pick(u), ur) <= TOL
+    if mode & 2:
+        assert rel(pick(v), vr) <= TOL
+    ug, vg = ser.evaluate_onsurface(*ser.to_device(node_block(blk)), delta, mode=mode)
+    if mode & 1:
+        assert rel(u.cpu().numpy(), ug.cpu().numpy()) <= 1e-13
+    if mode & 2:
+        assert rel(v.cpu().numpy(), vg.cpu().numpy()) <= 1e-13
