@@ -219,11 +219,11 @@ def run_reference(args, rank, world):
 
 def twodrop_launches(it: int) -> int:
     """Our kernel launches in one stokes_er_twodrop_solve that took `it` Krylov steps."""
-    per_eval = 7
-    n = 4 * per_eval + 2 + 2                # rhs: 4 block evals + 2 combines, norm (2)
+    per_blocks = 2 * (8 + 7)                # self block (node path, 8) + cross block (7) per drop
+    n = per_blocks + 2 + 2 + 1              # rhs: 4 block evals + 2 combines, norm (2), scale (1)
     for j in range(it):
-        n += 4 * per_eval + 2 + 2           # operator: 4 evals, 2 interpolations, 2 combines
-        n += 3 * (j + 1) + 3                # MGS: dot (2) + update (1) per basis vector; norm + scale
+        n += per_blocks + 2 + 2             # operator: 4 evals, 2 interpolations, 2 combines
+        n += 3 * (j + 1) + 3                # MGS: dot (2) + update (1) per basis vector; norm (2) + scale (1)
     return n + it                           # u = V y
 
 F_PROXY_ALG = 77  # algorithmic flops of one target-proxy interaction of eq. (31): a far pair's 57 with the

@@ -516,7 +516,10 @@ struct NodePlan {
   size_t off_tgt, off_orig, off_pacc, off_near, off_counter, total;
 };
 
-constexpr int kSymGrid = 148;  // persistent CTAs (one per B200 SM): fixed, so results do not depend on the device
+#ifndef SER_SYM_GRID
+#define SER_SYM_GRID 148
+#endif
+constexpr int kSymGrid = SER_SYM_GRID;  // persistent CTAs (one per B200 SM): fixed, so results do not depend on the device
 
 int64_t sym_items(int nsb, int k, int nchunks) {
   const int64_t qq = nsb / k;
@@ -532,7 +535,7 @@ NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
   p.nsb = static_cast<int>(ceil_div(p.nb, kSymWarps));
   // R blocks per item: the largest multiple of the warp count (<= 4 of them, SMEM) that still
   // gives every CTA >= 16 items (balance of the static assignment)
-  int k = 4;
+  int k = SER_SYM_MAXK;
   for (; k > 1; --k) {
     const int nch = static_cast<int>(ceil_div(p.nb, k * kSymWarps));
     if (sym_items(p.nsb, k, nch) >= 16 * kSymGrid) break;

@@ -37,6 +37,19 @@ constexpr int kBlkTileBytes = 2 * kNodeFields * 32 * 8;    // one R block in SME
 constexpr int kSymWarps = SER_SYM_WARPS;                   // I blocks per CTA (one per warp)
 constexpr int kSymThreads = kSymWarps * 32;
 constexpr int kSymStages = 3;                              // R-block TMA ring
+#ifndef SER_SYM_PIPE
+#define SER_SYM_PIPE 0                                     // software-pipelined step (measured slower)
+#endif
+#ifndef SER_SYM_UNROLL
+#define SER_SYM_UNROLL 4                                   // steps per loop iteration (2: -1%, 1: -1%)
+#endif
+constexpr int kSymUnroll = SER_SYM_UNROLL;
+#ifndef SER_SYM_MINB
+#define SER_SYM_MINB 1                                     // resident CTAs per SM (tuning macro)
+#endif
+#ifndef SER_SYM_MAXK
+#define SER_SYM_MAXK 4                                     // R blocks per item <= MAXK * warps (SMEM)
+#endif
 
 struct SymParams {
   const double* nsoa;     // [Npad/32][13][32]
@@ -164,11 +177,20 @@ __device__ __forceinline__ SymNode load_node(const double* __restrict__ t, int l
 // with S(d) g = g/r + d (d.g)/r^3 (eq. (3), even in d) and T(d) dq mw =
 // d (d.dq)(d.mw)/r^5 (eq. (4) without the -6, odd in d: the two sign flips of the
 // reverse direction cancel).  61 FP64 instructions for the two directed pairs
-// (41 for one directed pair in far_pair).
+// (41 for one directed pair in far_pair).  Split in two halves for the software
+// pipeline of sym_kernel: sym_geo (d and the MUFU + Newton 1/r, the long dependency
+// chain) of step k+1 is issued before sym_acc (the contractions) of step k.
+__device__ __forceinline__ Geo sym_geo(const SymNode& I, double rx, double ry, double rz) {
+  Geo g;
+  g.dx = I.x - rx;
+  g.dy = I.y - ry;
+  g.dz = I.z - rz;
+  g.ri = rsqrt_nr(fma(g.dx, g.dx, fma(g.dy, g.dy, g.dz * g.dz)));
+  return g;
+}
 template <int MODE>
-__device__ __forceinline__ void sym_pair(const SymNode& I, const SymNode& R, Acc& ai, Acc& ar) {
-  const double dx = I.x - R.x, dy = I.y - R.y, dz = I.z - R.z;
-  const double ri = rsqrt_nr(fma(dx, dx, fma(dy, dy, dz * dz)));
+__device__ __forceinline__ void sym_acc(const SymNode& I, const SymNode& R, const Geo& g, Acc& ai, Acc& ar) {
+  const double dx = g.dx, dy = g.dy, dz = g.dz, ri = g.ri;
   const double ri2 = ri * ri;
   if (MODE & 1) {
     const double gx = fma(-I.alpha, R.mx, R.fx), gy = fma(-I.alpha, R.my, R.fy), gz = fma(-I.alpha, R.mz, R.fz);
@@ -195,6 +217,10 @@ __device__ __forceinline__ void sym_pair(const SymNode& I, const SymNode& R, Acc
     ar.v2 = fma(dz, cr, ar.v2);
   }
 }
+template <int MODE>
+__device__ __forceinline__ void sym_pair(const SymNode& I, const SymNode& R, Acc& ai, Acc& ar) {
+  sym_acc<MODE>(I, R, sym_geo(I, R.x, R.y, R.z), ai, ar);
+}
 
 __device__ __forceinline__ void shfl_acc(Acc& a, int src_lane) {
   a.u0 = __shfl_sync(0xffffffffu, a.u0, src_lane);
@@ -215,7 +241,7 @@ __device__ __forceinline__ int64_t items_before(int64_t s, int k, int nchunks) {
 // Dynamic SMEM: R-block ring [kSymStages][2][13][32] | red [kSymWarps][6][64] |
 // chunk accumulator [6][chunk * 64].
 template <int MODE>
-__global__ void __launch_bounds__(kSymThreads, 1) sym_kernel(const SymParams p) {
+__global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const SymParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
   double* red = ring + kSymStages * 2 * kNodeFields * 32;
@@ -275,23 +301,64 @@ __global__ void __launch_bounds__(kSymThreads, 1) sym_kernel(const SymParams p) 
       const int n = r0 + ri;
       const bool active = has_i && n > myblk && blocks_far(p.blk_box, myblk, n, p.rc2_box);
       const double* R = ring + st * 2 * kNodeFields * 32;
-#pragma unroll 1
-      for (int hf = 0; hf < 2; ++hf) {
+      if (active) {
+#if SER_SYM_PIPE
+        // 64 steps over the R block's two 32-node halves; step kk pairs this lane's I nodes
+        // with R node (lane + kk) & 31 of half kk >> 5 (lane-varying, conflict-free SoA reads);
+        // the geometry of step kk + 1 is issued before the contractions of step kk (the last
+        // step recomputes step 0's and discards it)
+        auto rnode = [&](int kk) { return R + (kk >> 5) * kNodeFields * 32 + ((lane + kk) & 31); };
+        Geo g0, g1;
+        {
+          const double* t = rnode(0);
+          g0 = sym_geo(I0, t[NX * 32], t[NY * 32], t[NZ * 32]);
+          g1 = sym_geo(I1, t[NX * 32], t[NY * 32], t[NZ * 32]);
+        }
         Acc ra{0, 0, 0, 0, 0, 0};
-        if (active) {
-          const double* Rt = R + hf * kNodeFields * 32;
 #pragma unroll 2
+        for (int kk = 0; kk < 2 * 32; ++kk) {
+          const double* tn = rnode((kk + 1) & 63);
+          const Geo n0 = sym_geo(I0, tn[NX * 32], tn[NY * 32], tn[NZ * 32]);
+          const Geo n1 = sym_geo(I1, tn[NX * 32], tn[NY * 32], tn[NZ * 32]);
+          const double* t = rnode(kk);
+          SymNode rn;
+          rn.mx = t[NMX * 32]; rn.my = t[NMY * 32]; rn.mz = t[NMZ * 32];
+          if (MODE & 1) { rn.fx = t[NFX * 32]; rn.fy = t[NFY * 32]; rn.fz = t[NFZ * 32]; rn.alpha = t[NALPHA * 32]; }
+          if (MODE & 2) { rn.qx = t[NQX * 32]; rn.qy = t[NQY * 32]; rn.qz = t[NQZ * 32]; }
+          sym_acc<MODE>(I0, rn, g0, a0, ra);
+          sym_acc<MODE>(I1, rn, g1, a1, ra);
+          shfl_acc(ra, (lane + 1) & 31);  // lane l holds node (l + kk + 1) & 31 next
+          if ((kk & 31) == 31) {          // a half done: lane l holds R node (kk >> 5) * 32 + l
+            double* rw = red + warp * 6 * kBlk + (kk >> 5) * 32 + lane;
+            rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
+            rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
+            ra = Acc{0, 0, 0, 0, 0, 0};
+          }
+          g0 = n0;
+          g1 = n1;
+        }
+#else
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+          Acc ra{0, 0, 0, 0, 0, 0};
+          const double* Rt = R + hf * kNodeFields * 32;
+#pragma unroll kSymUnroll
           for (int kk = 0; kk < 32; ++kk) {
             const SymNode rn = load_node<MODE>(Rt, (lane + kk) & 31);
             sym_pair<MODE>(I0, rn, a0, ra);
             sym_pair<MODE>(I1, rn, a1, ra);
             shfl_acc(ra, (lane + 1) & 31);  // lane l holds node (l + kk + 1) & 31 next
           }
+          // lane l holds R node hf * 32 + l
+          double* rw = red + warp * 6 * kBlk + hf * 32 + lane;
+          rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
+          rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
         }
-        // lane l holds R node hf * 32 + l
-        double* rw = red + warp * 6 * kBlk + hf * 32 + lane;
-        rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
-        rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
+#endif
+      } else {  // inactive warp: its share of this R block is zero
+        double* rw = red + warp * 6 * kBlk + lane;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) { rw[c * kBlk] = 0.0; rw[c * kBlk + 32] = 0.0; }
       }
       __syncthreads();  // red complete; every warp is done reading ring[st]
       if (tid == 0 && ri + kSymStages < nr) {  // refill the stage just released
