@@ -761,7 +761,9 @@ def run_eval(args, rank, world):
     fused = args.schedule != "separate"
     opt.schedule = {"fused": 0, "separate": 1}[args.schedule]
     L = ser._lib.load()
-    nodes = args.path == "nodes" or (args.path == "auto" and args.config == 5 and world == 1)
+    # auto: the node path for config 5 on one GPU from N ~ 1.5e5 on (below that the general path is faster:
+    # 1/h = 64: 17.8 vs 15.9 ms; 1/h = 128: 204 vs 211 ms; 1/h = 256: 2.93 vs 3.25 s)
+    nodes = args.path == "nodes" or (args.path == "auto" and args.config == 5 and world == 1 and N >= 150000)
     if nodes and (world > 1 or args.config != 5):
         raise SystemExit("--path nodes: node-target workloads (config 5) on one GPU")
     if nodes:

@@ -156,7 +156,10 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override, int ph
   const int64_t nominal_ctas = 148 * (16 * 32 / kThreads);  // 16 resident warps per SM
   int64_t want = ceil_div(24 * nominal_ctas, p.n_tblocks);
   const int64_t mem_cap = std::max<int64_t>(1, (int64_t)(kPartialCapBytes / (48.0 * (double)p.Mpad)));
-  const int64_t min_tiles = std::max(1, 512 / kTile);  // >= 512 sources per item
+  // >= 512 sources per item, unless that leaves fewer than two waves of items (small problems,
+  // e.g. config 1: the critical path is then one item's loop): 128-source items
+  int64_t min_tiles = std::max(1, 512 / kTile);
+  if ((int64_t)p.n_tblocks * ceil_div(p.n_tiles, min_tiles) < 2 * nominal_ctas) min_tiles = 1;
   const int64_t max_chunks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.n_tiles, min_tiles), mem_cap));
   want = std::min<int64_t>(std::max<int64_t>(want, 1), max_chunks);
   p.chunk_tiles = static_cast<int>(ceil_div(p.n_tiles, want));
@@ -187,7 +190,9 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override, int ph
   p.off_partial = take((size_t)p.n_items * 6 * TB * sizeof(double));
   // near units (32-target group, phase): >= ~4 per resident warp (148 SMs x 12 warps)
   const int64_t groups = p.Mpad / 32;
-  p.near_phases = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));
+  // (up to 64 phases when there are few groups: small M)
+  p.near_phases = static_cast<int>(std::min<int64_t>(groups >= 512 ? 16 : 64,
+                                                     std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));
   if (phases_override > 0) p.near_phases = std::min(phases_override, 64);
   p.off_near = take((size_t)p.near_phases * p.Mpad * 6 * sizeof(double));
   p.off_counter = take(sizeof(int) * 4);
@@ -221,8 +226,11 @@ int check_arch() {
   return major == 10 ? STOKES_ER_OK : STOKES_ER_EARCH;
 }
 
-int opt_T(const stokes_er_options* o) {
-  return (o && o->targets_per_thread >= 1 && o->targets_per_thread <= 4) ? o->targets_per_thread : 2;
+int opt_T(const stokes_er_options* o, int64_t M = -1) {
+  if (o && o->targets_per_thread >= 1 && o->targets_per_thread <= 4) return o->targets_per_thread;
+  // default 2 targets per thread; 1 for tiny M (fewer than 37 blocks of 128 targets, e.g. config 1's 504):
+  // twice the target blocks for the critical path of a problem far smaller than the GPU
+  return (M >= 0 && ceil_div(M, (int64_t)kThreads * 2) < 37) ? 1 : 2;
 }
 int opt_chunk(const stokes_er_options* o) { return o ? o->source_chunk_tiles : 0; }
 int opt_phases(const stokes_er_options* o) { return o ? o->near_phases : 0; }
@@ -521,9 +529,10 @@ struct NodePlan {
 #endif
 constexpr int kSymGrid = SER_SYM_GRID;  // persistent CTAs (one per B200 SM): fixed, so results do not depend on the device
 
-int64_t sym_items(int nsb, int k, int nchunks) {
-  const int64_t qq = nsb / k;
-  return (int64_t)nsb * nchunks - ((int64_t)k * qq * (qq - 1) / 2 + qq * (nsb - qq * k));
+int64_t sym_items(int nsb, int k, int nchunks) {  // sum over chunks c of min(nsb, (c + 1) k)
+  int64_t n = 0;
+  for (int c = 0; c < nchunks; ++c) n += std::min<int64_t>(nsb, (int64_t)(c + 1) * k);
+  return n;
 }
 
 NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
@@ -700,7 +709,7 @@ size_t stokes_er_workspace_bytes(int64_t M, int64_t N, int mode) {
 size_t stokes_er_workspace_bytes_ex(int64_t M, int64_t N, int mode, const stokes_er_options* options) {
   if (M < 0 || N < 1 || mode < 1 || mode > 3) return 0;
   return std::max(stokes_er_workspace_bytes(M, N, mode),
-                  make_plan(M, N, mode, opt_T(options), opt_chunk(options), opt_phases(options)).total);
+                  make_plan(M, N, mode, opt_T(options, M), opt_chunk(options), opt_phases(options)).total);
 }
 
 static int eval_common(const double* src_xyz, const double* src_normal, const double* src_weight, const double* f,
@@ -714,7 +723,7 @@ static int eval_common(const double* src_xyz, const double* src_normal, const do
   if (M == 0) return STOKES_ER_OK;
   if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
   if ((st = check_arch())) return st;
-  const Plan P = make_plan(M, N, mode, opt_T(options), opt_chunk(options), opt_phases(options));
+  const Plan P = make_plan(M, N, mode, opt_T(options, M), opt_chunk(options), opt_phases(options));
   if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* ws = static_cast<char*>(workspace);

@@ -231,11 +231,13 @@ __device__ __forceinline__ void shfl_acc(Acc& a, int src_lane) {
   a.v2 = __shfl_sync(0xffffffffu, a.v2, src_lane);
 }
 
-// item -> (superblock s, chunk c): superblock s pairs with chunks c >= s / k
-// (k = chunk / kSymWarps superblocks per chunk); items are numbered s-major.
-__device__ __forceinline__ int64_t items_before(int64_t s, int k, int nchunks) {
-  const int64_t qq = s / k;  // sum_{s' < s} floor(s'/k) = k q(q-1)/2 + q (s - q k)
-  return s * nchunks - (k * qq * (qq - 1) / 2 + qq * (s - qq * k));
+// item -> (chunk c, superblock s): chunk c pairs with superblocks s < (c + 1) k (k = chunk /
+// kSymWarps superblocks per chunk), i.e. min(nsb, (c + 1) k) items; items are numbered c-major,
+// so a CTA's contiguous range of items mostly shares one chunk and its R sums stay in SMEM.
+__device__ __forceinline__ int64_t items_before(int64_t c, int k, int nsb) {
+  const int64_t cs = nsb / k;  // chunks c' < cs have (c' + 1) k <= nsb superblocks
+  if (c <= cs) return (int64_t)k * c * (c + 1) / 2;
+  return (int64_t)k * cs * (cs + 1) / 2 + (c - cs) * nsb;
 }
 
 // Dynamic SMEM: R-block ring [kSymStages][2][13][32] | red [kSymWarps][6][64] |
@@ -258,16 +260,32 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
   __syncthreads();
   uint32_t phase_bits = 0;
   double* my_acc = p.pacc + (int64_t)blockIdx.x * 6 * p.Npad;
+  // this CTA's contiguous range of the c-major item list (static: deterministic sums)
+  const int64_t item_lo = (int64_t)blockIdx.x * p.n_items / G, item_hi = ((int64_t)blockIdx.x + 1) * p.n_items / G;
+  int cur_c = -1;
+  auto flush_chunk = [&](int c) {  // the chunk's R sums into this CTA's slice
+    const int r0 = c * p.chunk, nr = min(p.chunk, p.nb - r0);
+    for (int x = tid; x < 6 * nr * kBlk; x += kSymThreads) {
+      const int comp = x / (nr * kBlk), col = x - comp * (nr * kBlk);
+      my_acc[comp * p.Npad + (int64_t)r0 * kBlk + col] += cacc[comp * cw + col];
+    }
+  };
 
-  for (int64_t item = blockIdx.x; item < p.n_items; item += G) {
-    // item -> (s, c): binary search on the s-major prefix counts
-    int64_t lo = 0, hi = p.nsb - 1;
+  for (int64_t item = item_lo; item < item_hi; ++item) {
+    // item -> (c, s): binary search on the c-major prefix counts
+    int64_t lo = 0, hi = p.nchunks - 1;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
-      if (items_before(mid, k, p.nchunks) <= item) lo = mid; else hi = mid - 1;
+      if (items_before(mid, k, p.nsb) <= item) lo = mid; else hi = mid - 1;
     }
-    const int s = static_cast<int>(lo);
-    const int c = static_cast<int>(s / k + (item - items_before(lo, k, p.nchunks)));
+    const int c = static_cast<int>(lo);
+    const int s = static_cast<int>(item - items_before(lo, k, p.nsb));
+    if (c != cur_c) {  // a new chunk: flush the previous one's R sums, start from zero
+      if (cur_c >= 0) flush_chunk(cur_c);
+      __syncthreads();
+      for (int x = tid; x < 6 * cw; x += kSymThreads) cacc[x] = 0.0;
+      cur_c = c;
+    }
     const int myblk = s * kSymWarps + warp;
     const int r0 = c * p.chunk;
     const int nr = min(p.chunk, p.nb - r0);
@@ -284,8 +302,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       I0 = load_node<MODE>(t, lane);
       I1 = load_node<MODE>(t + kNodeFields * 32, lane);
     }
-    for (int x = tid; x < 6 * cw; x += kSymThreads) cacc[x] = 0.0;
-    __syncthreads();  // cacc zeroed; the previous item's readers of the ring are done
+    __syncthreads();  // cacc ready; the previous item's readers of the ring are done
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       for (int b = 0; b < kSymStages && first + b < nr; ++b) {
@@ -376,7 +393,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       }
       __syncthreads();  // red may be overwritten
     }
-    // flush: I sums of every warp, then the chunk's R sums (both into this CTA's slice, in order)
+    // flush: the I sums of every warp into this CTA's slice (the chunk's R sums when the chunk changes)
     if (has_i) {
       const int64_t i0 = (int64_t)myblk * kBlk + lane, i1 = i0 + 32;
       double* a = my_acc;
@@ -385,13 +402,9 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       a[0 * p.Npad + i1] += a1.u0; a[1 * p.Npad + i1] += a1.u1; a[2 * p.Npad + i1] += a1.u2;
       a[3 * p.Npad + i1] += a1.v0; a[4 * p.Npad + i1] += a1.v1; a[5 * p.Npad + i1] += a1.v2;
     }
-    __syncthreads();  // I flush before the R flush (a diagonal chunk holds the same nodes)
-    for (int x = tid; x < 6 * nr * kBlk; x += kSymThreads) {
-      const int comp = x / (nr * kBlk), col = x - comp * (nr * kBlk);
-      my_acc[comp * p.Npad + (int64_t)r0 * kBlk + col] += cacc[comp * cw + col];
-    }
-    __syncthreads();
+    __syncthreads();  // I flush before any R flush (a diagonal chunk holds the same nodes)
   }
+  if (cur_c >= 0) flush_chunk(cur_c);
 }
 
 // ---------------------------------------------------------------- K6

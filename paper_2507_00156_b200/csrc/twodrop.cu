@@ -18,9 +18,20 @@ namespace twodrop {
 
 constexpr int kKmax = STOKES_ER_INTERP_KMAX;  // stencil capacity
 constexpr int kRowsPerLane = kKmax / 32;      // stencil rows held by each lane
-constexpr int kNpoly = 15;                    // monomials of total degree <= 4 in 2 variables
-constexpr double kInterpRadius = 3.5;         // stencil: nodes within 3.5 h of x0 (R20)
+#ifndef SER_INTERP_DEG
+#define SER_INTERP_DEG 4                      // R20: total degree of the cross-point polynomial (study: DESIGN 5.5)
+#endif
+#ifndef SER_INTERP_RADIUS
+#define SER_INTERP_RADIUS 3.5                 // R20: stencil = nodes within this many h of x0
+#endif
+constexpr int kInterpDeg = SER_INTERP_DEG;
+constexpr int kNpoly = (kInterpDeg + 1) * (kInterpDeg + 2) / 2;  // monomials of total degree <= kInterpDeg
+constexpr double kInterpRadius = SER_INTERP_RADIUS;
 constexpr int kDotBlocks = 296;
+#ifndef SER_NODES_MIN_N
+#define SER_NODES_MIN_N 150000                // self blocks through stokes_er_eval_nodes_onsurface from here on
+#endif
+constexpr int64_t kNodesMinN = SER_NODES_MIN_N;
 static_assert(kKmax % 32 == 0, "stencil capacity: whole warps");
 
 // ----------------------------------------------------------------- kernels
@@ -93,7 +104,7 @@ __global__ void stencil_kernel(const double* __restrict__ sx, int64_t Ns, const 
       on = 1.0;
     }
     int c = 0;
-    for (int deg = 0; deg <= 4; ++deg)
+    for (int deg = 0; deg <= kInterpDeg; ++deg)
       for (int pb = 0; pb <= deg; ++pb) {
         double v = on;
         for (int i = 0; i < deg - pb; ++i) v *= xi;
@@ -325,10 +336,15 @@ int blocks(const Ctx& c, int mode, const double* u, double* out) {
                                          sl ? nullptr : ub, d[b].xyz, c.at<double>(c.L.off_zero[b]), x0s, Nb, Nb,
                                          c.P->delta_self, mode, c.P->tree, c.P->tree_plan[b], sl ? vs : nullptr,
                                          sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
-    else  // the self block's targets are the drop's own nodes: the symmetric node path (same sums)
+    else if (Nb >= kNodesMinN)  // the self block's targets are the drop's own nodes: the symmetric node
+                                // path (same sums; faster from ~1.5e5 nodes)
       st = stokes_er_eval_nodes_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr,
                                           sl ? nullptr : ub, Nb, c.P->delta_self, mode, sl ? vs : nullptr,
                                           sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
+    else
+      st = stokes_er_eval_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr, sl ? nullptr : ub,
+                                    d[b].xyz, c.at<double>(c.L.off_zero[b]), x0s, Nb, Nb, c.P->delta_self, mode,
+                                    sl ? vs : nullptr, sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
     if (st) break;
     if (c.P->use_tree)
       st = stokes_er_eval_tree(d[m].xyz, d[m].normal, d[m].weight, sl ? d[m].f : nullptr, sl ? nullptr : um,
