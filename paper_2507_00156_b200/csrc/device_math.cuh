@@ -75,14 +75,16 @@ __device__ __forceinline__ void s_factors(double t, double& s1, double& s2, doub
   s3 = s2 - c23;
 }
 
-// e^{-u} for 0 <= u <= 700: Cody-Waite reduction u = n ln2 + r, |r| <= ln2/2,
-// degree-11 polynomial (tools/gen_sfactor_coeffs.py), scale 2^n by building the
-// exponent bits.  No special-case branches; u > ~708 would overflow the exponent
-// field, so callers clamp u (e^{-700} ~ 1e-304 is below every contribution).
+// e^{-u} for u >= 0: Cody-Waite reduction u = n ln2 + r, |r| <= ln2/2, degree-11
+// polynomial (tools/gen_sfactor_coeffs.py), scale 2^n by building the exponent
+// bits.  No special-case branches.  For u > ~708 the exponent field would
+// underflow: n is clamped at -1022 (an integer max, off the FP64 pipe), which
+// returns a value below 2e-308 -- 0 to every sum it enters -- instead of e^{-u}.
+// (t = r/delta_k reaches 6 rho_3/rho_1 on a near pair: u > 708 once rho_3/rho_1 > 4.4.)
 __device__ __forceinline__ double exp_neg(double u) {
   const double x = -u;
   const double kd = fma(x, 1.4426950408889634074, 6755399441055744.0);  // round(x/ln2) + 1.5*2^52
-  const int n = __double2loint(kd);
+  const int n = max(__double2loint(kd), -1022);
   const double nd = kd - 6755399441055744.0;
   double r = fma(nd, -6.93147180559945286227e-01, x);
   r = fma(nd, -2.31904681384629955842e-17, r);
@@ -108,9 +110,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // Branch-free, no tables; for t < 0.5 it returns finite values the caller discards.
 __device__ __forceinline__ void sfactor_s(double t, double& E, double& s2, double& c23, double* e_out = nullptr) {
   const double u = t * t;
-  // t = r/delta_k can reach 6 rho_3/rho_1 on a near pair (t^2 > 700 once
-  // rho_3/rho_1 > 4.4): clamp so exp_neg stays in range; e^{-700} is 0 to the sums
-  const double e = exp_neg(fmin(u, 700.0));
+  const double e = exp_neg(u);  // any u >= 0 (exp_neg clamps its exponent)
   if (e_out) *e_out = e;  // e^{-t^2}, for callers that need it too (the s# factors)
   const double tc = fmin(t, 6.0);  // erfc(t > 6) < 2e-17: E rounds to 1 either way
   const double x = fma(rcp_nr(kErfcxKappa + tc), kErfcxVA, kErfcxVB);

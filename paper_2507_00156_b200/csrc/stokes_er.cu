@@ -573,7 +573,7 @@ NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
   p.off_src = take(p.Npad * kSrcDoubles * sizeof(double));
   p.off_srcbox = take((p.Npad / kSub + p.Npad / 16) * 8 * sizeof(double));
   p.off_blkbox = take((size_t)p.nb * 8 * sizeof(double));
-  p.off_nsoa = take(p.Npad * kNodeFields * sizeof(double));
+  p.off_nsoa = take(p.Npad * kNodeStride * sizeof(double));
   p.off_tgt = take(p.Npad * kTgtFields * sizeof(double));
   p.off_orig = take(p.Npad * sizeof(int32_t));
   p.off_pacc = take((size_t)p.G * 6 * p.Npad * sizeof(double));

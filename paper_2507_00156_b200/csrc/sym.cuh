@@ -27,10 +27,18 @@
 
 namespace ser {
 
-constexpr int kNodeFields = 13;  // SoA tile rows: x y z | mx my mz | fx fy fz | qx qy qz | alpha
+constexpr int kNodeFields = 13;  // x y z | mx my mz | fx fy fz | qx qy qz | alpha
 enum NodeField { NX = 0, NY, NZ, NMX, NMY, NMZ, NFX, NFY, NFZ, NQX, NQY, NQZ, NALPHA };
+#ifndef SER_SYM_AOS
+#define SER_SYM_AOS 1  // node records of 14 doubles (13 + pad, 112 B) instead of SoA 32-node tiles
+#endif
+// AoS: lane-varying 16-byte reads of record (l + k) mod 32 are conflict-free (112 B = 28 banks:
+// 8 consecutive records start on 8 distinct 4-bank groups), 7 LDS.128 per node instead of 13 LDS.64
+constexpr int kNodeStride = SER_SYM_AOS ? 14 : kNodeFields;       // doubles per node in a tile
+constexpr int kTileDoubles = 32 * kNodeStride;                     // one 32-node tile
+__host__ __device__ constexpr int nfield(int l, int f) { return SER_SYM_AOS ? l * 14 + f : f * 32 + l; }
 constexpr int kBlk = 64;                                   // nodes per symmetric block (2 sub-tiles)
-constexpr int kBlkTileBytes = 2 * kNodeFields * 32 * 8;    // one R block in SMEM (TMA unit): 6656 B
+constexpr int kBlkTileBytes = 2 * kTileDoubles * 8;        // one R block in SMEM (TMA unit)
 #ifndef SER_SYM_WARPS
 #define SER_SYM_WARPS 12
 #endif
@@ -104,15 +112,17 @@ __global__ void pack_node_soa(const double* __restrict__ xyz, const double* __re
     qv[d] = (MODE & 2) ? q[d * N + j] : 0.0;
   }
   const double alpha = fma(fv[0], n[0], fma(fv[1], n[1], fv[2] * n[2]));  // f(x0).n0
-  double* t = nsoa + (i >> 5) * (kNodeFields * 32) + (i & 31);
+  double* t = nsoa + (i >> 5) * kTileDoubles;
+  const int l = static_cast<int>(i & 31);
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    t[(NX + d) * 32] = x[d];
-    t[(NMX + d) * 32] = n[d] * w;
-    t[(NFX + d) * 32] = fv[d] * w;
-    t[(NQX + d) * 32] = qv[d];
+    t[nfield(l, NX + d)] = x[d];
+    t[nfield(l, NMX + d)] = n[d] * w;
+    t[nfield(l, NFX + d)] = fv[d] * w;
+    t[nfield(l, NQX + d)] = qv[d];
   }
-  t[NALPHA * 32] = alpha;
+  t[nfield(l, NALPHA)] = alpha;
+  if (SER_SYM_AOS) t[nfield(l, 13)] = 0.0;
   double wk[3] = {1.0, 0.0, 0.0};  // NEXT-1 (s#): one delta, no extrapolation
   if (!sharp) extrap_weights(0.0, h, rho.rho, STOKES_ER_CUTOFF, wk);
   tgt[F_Y0 * Npad + i] = x[0];
@@ -155,6 +165,23 @@ struct SymNode {
 template <int MODE>
 __device__ __forceinline__ SymNode load_node(const double* __restrict__ t, int l) {
   SymNode n;
+#if SER_SYM_AOS
+  const double2* p = reinterpret_cast<const double2*>(t + l * kNodeStride);
+  const double2 a = p[0], b = p[1], c = p[2];
+  n.x = a.x; n.y = a.y; n.z = b.x; n.mx = b.y; n.my = c.x; n.mz = c.y;
+  if (MODE & 1) {
+    const double2 d = p[3], e = p[4], g = p[6];
+    n.fx = d.x; n.fy = d.y; n.fz = e.x; n.alpha = g.x;
+  } else {
+    n.fx = n.fy = n.fz = n.alpha = 0.0;
+  }
+  if (MODE & 2) {
+    const double2 e = p[4], f = p[5];
+    n.qx = e.y; n.qy = f.x; n.qz = f.y;
+  } else {
+    n.qx = n.qy = n.qz = 0.0;
+  }
+#else
   n.x = t[NX * 32 + l]; n.y = t[NY * 32 + l]; n.z = t[NZ * 32 + l];
   n.mx = t[NMX * 32 + l]; n.my = t[NMY * 32 + l]; n.mz = t[NMZ * 32 + l];
   if (MODE & 1) {
@@ -168,6 +195,7 @@ __device__ __forceinline__ SymNode load_node(const double* __restrict__ t, int l
   } else {
     n.qx = n.qy = n.qz = 0.0;
   }
+#endif
   return n;
 }
 
@@ -246,7 +274,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const SymParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
-  double* red = ring + kSymStages * 2 * kNodeFields * 32;
+  double* red = ring + kSymStages * 2 * kTileDoubles;
   double* cacc = red + kSymWarps * 6 * kBlk;
   __shared__ __align__(8) uint64_t bar[kSymStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -298,16 +326,16 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
     SymNode I0, I1;
     Acc a0{0, 0, 0, 0, 0, 0}, a1{0, 0, 0, 0, 0, 0};
     if (has_i) {
-      const double* t = p.nsoa + (int64_t)(2 * myblk) * kNodeFields * 32;
+      const double* t = p.nsoa + (int64_t)(2 * myblk) * kTileDoubles;
       I0 = load_node<MODE>(t, lane);
-      I1 = load_node<MODE>(t + kNodeFields * 32, lane);
+      I1 = load_node<MODE>(t + kTileDoubles, lane);
     }
     __syncthreads();  // cacc ready; the previous item's readers of the ring are done
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       for (int b = 0; b < kSymStages && first + b < nr; ++b) {
         mbar_expect_tx(&bar[b], kBlkTileBytes);
-        bulk_g2s(ring + b * 2 * kNodeFields * 32, p.nsoa + (int64_t)(2 * (r0 + first + b)) * kNodeFields * 32,
+        bulk_g2s(ring + b * 2 * kTileDoubles, p.nsoa + (int64_t)(2 * (r0 + first + b)) * kTileDoubles,
                  kBlkTileBytes, &bar[b]);
       }
     }
@@ -317,31 +345,31 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       phase_bits ^= 1u << st;
       const int n = r0 + ri;
       const bool active = has_i && n > myblk && blocks_far(p.blk_box, myblk, n, p.rc2_box);
-      const double* R = ring + st * 2 * kNodeFields * 32;
+      const double* R = ring + st * 2 * kTileDoubles;
       if (active) {
 #if SER_SYM_PIPE
         // 64 steps over the R block's two 32-node halves; step kk pairs this lane's I nodes
         // with R node (lane + kk) & 31 of half kk >> 5 (lane-varying, conflict-free SoA reads);
         // the geometry of step kk + 1 is issued before the contractions of step kk (the last
         // step recomputes step 0's and discards it)
-        auto rnode = [&](int kk) { return R + (kk >> 5) * kNodeFields * 32 + ((lane + kk) & 31); };
+        auto rnode = [&](int kk) { return R + (kk >> 5) * kTileDoubles + nfield((lane + kk) & 31, 0); };
         Geo g0, g1;
         {
           const double* t = rnode(0);
-          g0 = sym_geo(I0, t[NX * 32], t[NY * 32], t[NZ * 32]);
-          g1 = sym_geo(I1, t[NX * 32], t[NY * 32], t[NZ * 32]);
+          g0 = sym_geo(I0, t[nfield(0, NX)], t[nfield(0, NY)], t[nfield(0, NZ)]);
+          g1 = sym_geo(I1, t[nfield(0, NX)], t[nfield(0, NY)], t[nfield(0, NZ)]);
         }
         Acc ra{0, 0, 0, 0, 0, 0};
 #pragma unroll 2
         for (int kk = 0; kk < 2 * 32; ++kk) {
           const double* tn = rnode((kk + 1) & 63);
-          const Geo n0 = sym_geo(I0, tn[NX * 32], tn[NY * 32], tn[NZ * 32]);
-          const Geo n1 = sym_geo(I1, tn[NX * 32], tn[NY * 32], tn[NZ * 32]);
+          const Geo n0 = sym_geo(I0, tn[nfield(0, NX)], tn[nfield(0, NY)], tn[nfield(0, NZ)]);
+          const Geo n1 = sym_geo(I1, tn[nfield(0, NX)], tn[nfield(0, NY)], tn[nfield(0, NZ)]);
           const double* t = rnode(kk);
           SymNode rn;
-          rn.mx = t[NMX * 32]; rn.my = t[NMY * 32]; rn.mz = t[NMZ * 32];
-          if (MODE & 1) { rn.fx = t[NFX * 32]; rn.fy = t[NFY * 32]; rn.fz = t[NFZ * 32]; rn.alpha = t[NALPHA * 32]; }
-          if (MODE & 2) { rn.qx = t[NQX * 32]; rn.qy = t[NQY * 32]; rn.qz = t[NQZ * 32]; }
+          rn.mx = t[nfield(0, NMX)]; rn.my = t[nfield(0, NMY)]; rn.mz = t[nfield(0, NMZ)];
+          if (MODE & 1) { rn.fx = t[nfield(0, NFX)]; rn.fy = t[nfield(0, NFY)]; rn.fz = t[nfield(0, NFZ)]; rn.alpha = t[nfield(0, NALPHA)]; }
+          if (MODE & 2) { rn.qx = t[nfield(0, NQX)]; rn.qy = t[nfield(0, NQY)]; rn.qz = t[nfield(0, NQZ)]; }
           sym_acc<MODE>(I0, rn, g0, a0, ra);
           sym_acc<MODE>(I1, rn, g1, a1, ra);
           shfl_acc(ra, (lane + 1) & 31);  // lane l holds node (l + kk + 1) & 31 next
@@ -358,7 +386,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
 #pragma unroll 1
         for (int hf = 0; hf < 2; ++hf) {
           Acc ra{0, 0, 0, 0, 0, 0};
-          const double* Rt = R + hf * kNodeFields * 32;
+          const double* Rt = R + hf * kTileDoubles;
 #pragma unroll kSymUnroll
           for (int kk = 0; kk < 32; ++kk) {
             const SymNode rn = load_node<MODE>(Rt, (lane + kk) & 31);
@@ -381,7 +409,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       if (tid == 0 && ri + kSymStages < nr) {  // refill the stage just released
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[st], kBlkTileBytes);
-        bulk_g2s(ring + st * 2 * kNodeFields * 32, p.nsoa + (int64_t)(2 * (n + kSymStages)) * kNodeFields * 32,
+        bulk_g2s(ring + st * 2 * kTileDoubles, p.nsoa + (int64_t)(2 * (n + kSymStages)) * kTileDoubles,
                  kBlkTileBytes, &bar[st]);
       }
       for (int x = tid; x < 6 * kBlk; x += kSymThreads) {  // fixed warp order: deterministic

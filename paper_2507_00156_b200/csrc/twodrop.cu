@@ -29,7 +29,7 @@ constexpr int kNpoly = (kInterpDeg + 1) * (kInterpDeg + 2) / 2;  // monomials of
 constexpr double kInterpRadius = SER_INTERP_RADIUS;
 constexpr int kDotBlocks = 296;
 #ifndef SER_NODES_MIN_N
-#define SER_NODES_MIN_N 150000                // self blocks through stokes_er_eval_nodes_onsurface from here on
+#define SER_NODES_MIN_N 50000                 // self blocks through stokes_er_eval_nodes_onsurface from here on
 #endif
 constexpr int64_t kNodesMinN = SER_NODES_MIN_N;
 static_assert(kKmax % 32 == 0, "stencil capacity: whole warps");
@@ -337,7 +337,7 @@ int blocks(const Ctx& c, int mode, const double* u, double* out) {
                                          c.P->delta_self, mode, c.P->tree, c.P->tree_plan[b], sl ? vs : nullptr,
                                          sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
     else if (Nb >= kNodesMinN)  // the self block's targets are the drop's own nodes: the symmetric node
-                                // path (same sums; faster from ~1.5e5 nodes)
+                                // path (same sums; measured 498 vs 515 ms per solve at 1/h = 64)
       st = stokes_er_eval_nodes_onsurface(d[b].xyz, d[b].normal, d[b].weight, sl ? d[b].f : nullptr,
                                           sl ? nullptr : ub, Nb, c.P->delta_self, mode, sl ? vs : nullptr,
                                           sl ? nullptr : vs, ews, c.L.eval_ws, c.s);
