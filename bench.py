@@ -616,8 +616,9 @@ def committed_traffic(bench_cfg: dict, kernel_prefix: str):
         meta = d.get("bench_config")
         if not meta or any(meta.get(k) != bench_cfg.get(k) for k in keys):
             continue
+        want = kernel_prefix.replace("ser::", "")  # ncu's raw page prints the name without the namespace
         for k in d.get("kernels", []):
-            if k["kernel"].startswith(kernel_prefix) and "dram__bytes_read.sum" in k:
+            if k["kernel"].replace("ser::", "").startswith(want) and "dram__bytes_read.sum" in k:
                 tot = 0.0
                 for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     v, u = k[key].split()

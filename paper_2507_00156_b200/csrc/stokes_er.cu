@@ -499,12 +499,20 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   np.rc2_box = rc2 * (1.0 + 1e-9);
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = 1.0 / (rho[k] * h);
   {  // one persistent kernel: tree walks of the target groups + the near units
+    const int n_near = SER_TREE_FUSED_NEAR ? np.n_units : 0;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tree_far_kernel<MODE, SHARP>, kTreeWarps * 32, 0);
-    const int64_t work = (int64_t)tfp.n_groups + np.n_units;
+    const int64_t work = (int64_t)tfp.n_groups + n_near;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(work, kTreeWarps), (int64_t)sms * std::max(occ, 1))));
-    tree_far_kernel<MODE, SHARP><<<grid, kTreeWarps * 32, 0, s>>>(tfp, np, np.n_units);
+    tree_far_kernel<MODE, SHARP><<<grid, kTreeWarps * 32, 0, s>>>(tfp, np, n_near);
+    if (!SER_TREE_FUSED_NEAR) {
+      int nocc = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nocc, near_kernel<MODE, SHARP>, kNearWarps * 32, 0);
+      const int ngrid = static_cast<int>(std::max<int64_t>(
+          1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(nocc, 1))));
+      near_kernel<MODE, SHARP><<<ngrid, kNearWarps * 32, 0, s>>>(np);
+    }
   }
   finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad, 1, 32,
                                                           P.near_phases, out_u, out_v);

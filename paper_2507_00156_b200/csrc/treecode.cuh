@@ -34,6 +34,9 @@ constexpr int kTreeWarps = 4;             // warps per CTA of tree_far_kernel
 #ifndef SER_TREE_MINB
 #define SER_TREE_MINB 4
 #endif
+#ifndef SER_TREE_FUSED_NEAR
+#define SER_TREE_FUSED_NEAR 1  // near units interleaved in the walk kernel's queue (0: separate near_kernel)
+#endif
 constexpr uint64_t kTreeMagic = 0x53455254524545ULL;  // "SERTREE"
 
 struct TreeNode {  // POD, identical on host and device
@@ -316,10 +319,14 @@ __global__ void __launch_bounds__(kTreeWarps * 32, SER_TREE_MINB) tree_far_kerne
     qi = __shfl_sync(0xffffffffu, qi, 0);
     if (qi >= total) break;
     int64_t idx;
+#if SER_TREE_FUSED_NEAR
     if (fused_slot(qi, p.n_groups, n_near, &idx)) {
       near_unit<MODE, SHARP>(np, static_cast<int>(idx), s_all[warp].n);
       continue;
     }
+#else
+    idx = qi;  // walk only: the near units run in near_kernel
+#endif
     const int g = static_cast<int>(idx);
     __syncwarp();
     if (lane <= p.p) sm.cosk[lane] = cos(lane * kPi / p.p);
@@ -351,6 +358,7 @@ __global__ void __launch_bounds__(kTreeWarps * 32, SER_TREE_MINB) tree_far_kerne
         const double R2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
         const double yv[3] = {t.y0, t.y1, t.y2};
         double g2 = 0.0;
+#pragma unroll
         for (int d = 0; d < 3; ++d) {
           double gap = __dadd_rn(nd.lo[d], -yv[d]);
           const double up = __dadd_rn(yv[d], -nd.hi[d]);
