@@ -153,7 +153,8 @@ int stokes_er_eval_onsurface(const double* src_xyz, const double* src_normal, co
                              double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
                              void* stream);
 
-/* Number of kernel launches one stokes_er_eval(M, N, mode) enqueues. */
+/* Number of kernel launches one stokes_er_eval(M, N, mode) enqueues (ours; 4 when N, M <= 16384: the
+ * one-CTA sort prologue; 7 otherwise, plus the CUB radix-sort launches). */
 int stokes_er_launch_count(int64_t M, int64_t N, int mode);
 
 /* Optional profiling hooks for bench.py: if non-NULL, cudaEvent_t handles

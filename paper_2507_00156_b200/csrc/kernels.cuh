@@ -33,6 +33,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdint>
 #include <cstring>
@@ -183,32 +184,105 @@ __global__ void bbox_kernel(const double* __restrict__ sx, int64_t N, const doub
   }
 }
 
+// 30-bit Morton key of point i of x [3][n] in the box (blo, bhi).
+__device__ __forceinline__ uint32_t morton_key(const double* __restrict__ x, int64_t n, int64_t i,
+                                               const double (&blo)[3], const double (&bhi)[3]) {
+  uint32_t key = 0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double ext = fmax(bhi[d] - blo[d], 1e-300);
+    double s = (x[d * n + i] - blo[d]) / ext * 1023.0;
+    s = fmin(fmax(s, 0.0), 1023.0);
+    key |= spread10(static_cast<uint32_t>(s)) << d;
+  }
+  return key;
+}
+
 __global__ void morton_kernel(const double* __restrict__ x, int64_t n, const long long* __restrict__ box,
                               uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint32_t key = 0;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double blo = dkey_inv(box[d]), bhi = dkey_inv(box[3 + d]);
-    const double ext = fmax(bhi - blo, 1e-300);
-    double s = (x[d * n + i] - blo) / ext * 1023.0;
-    s = fmin(fmax(s, 0.0), 1023.0);
-    key |= spread10(static_cast<uint32_t>(s)) << d;
-  }
-  keys[i] = key;
+  const double blo[3] = {dkey_inv(box[0]), dkey_inv(box[1]), dkey_inv(box[2])};
+  const double bhi[3] = {dkey_inv(box[3]), dkey_inv(box[4]), dkey_inv(box[5])};
+  keys[i] = morton_key(x, n, i, blo, bhi);
   vals[i] = static_cast<int32_t>(i);
+}
+
+// Small problems (N, M <= kSmallSort): bounding box, Morton keys and a stable radix sort of
+// sources and of targets in ONE CTA (the same keys and the same stable order as bbox_kernel +
+// morton_kernel + the CUB device sorts, so the same sums), instead of ~15 launches.
+constexpr int kSmallSortThreads = 1024, kSmallSortItems = 16;
+constexpr int64_t kSmallSort = (int64_t)kSmallSortThreads * kSmallSortItems;
+constexpr int kSmallSortSmem =
+    (int)sizeof(typename cub::BlockRadixSort<uint32_t, kSmallSortThreads, kSmallSortItems, int32_t>::TempStorage);
+__global__ void __launch_bounds__(kSmallSortThreads, 1) small_sort_kernel(const double* __restrict__ sx, int64_t N,
+                                                                         const double* __restrict__ tx, int64_t M,
+                                                                         int32_t* __restrict__ svout,
+                                                                         int32_t* __restrict__ tvout) {
+  using Sort = cub::BlockRadixSort<uint32_t, kSmallSortThreads, kSmallSortItems, int32_t>;
+  extern __shared__ __align__(16) unsigned char small_smem[];  // kSmallSortSmem bytes (dynamic: > 48 KB)
+  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(small_smem);
+  __shared__ double red[kSmallSortThreads / 32][6];
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = threadIdx.x; i < N + M; i += kSmallSortThreads) {
+    const double* x = i < N ? sx + i : tx + (i - N);
+    const int64_t n = i < N ? N : M;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = fmin(lo[d], x[d * n]);
+      hi[d] = fmax(hi[d], x[d * n]);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    for (int o = 16; o; o >>= 1) {
+      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+    for (int d = 0; d < 3; ++d) { red[w][d] = lo[d]; red[w][3 + d] = hi[d]; }
+  __syncthreads();
+  double blo[3], bhi[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {  // every thread reduces the 32 warp results (min/max: exact, order-free)
+    blo[d] = red[0][d];
+    bhi[d] = red[0][3 + d];
+    for (int k = 1; k < kSmallSortThreads / 32; ++k) {
+      blo[d] = fmin(blo[d], red[k][d]);
+      bhi[d] = fmax(bhi[d], red[k][3 + d]);
+    }
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* x = pass == 0 ? sx : tx;
+    const int64_t n = pass == 0 ? N : M;
+    int32_t* out = pass == 0 ? svout : tvout;
+    uint32_t keys[kSmallSortItems];
+    int32_t vals[kSmallSortItems];
+#pragma unroll
+    for (int k = 0; k < kSmallSortItems; ++k) {  // blocked arrangement: thread t holds t*ITEMS + k
+      const int64_t i = (int64_t)threadIdx.x * kSmallSortItems + k;
+      keys[k] = i < n ? morton_key(x, n, i, blo, bhi) : 0x3fffffffu;  // padding sorts last (stable)
+      vals[k] = static_cast<int32_t>(i);
+    }
+    __syncthreads();  // tmp free
+    Sort(tmp).Sort(keys, vals, 0, 30);
+#pragma unroll
+    for (int k = 0; k < kSmallSortItems; ++k) {
+      const int64_t r = (int64_t)threadIdx.x * kSmallSortItems + k;
+      if (r < n) out[r] = vals[k];
+    }
+  }
 }
 
 // One warp per 32-source sub-tile: gather into AoS records and its bounding box.
 template <int MODE>
-__global__ void pack_sources(const double* __restrict__ xyz, const double* __restrict__ nrm,
-                             const double* __restrict__ wgt, const double* __restrict__ f,
-                             const double* __restrict__ q, int64_t N, int64_t Npad,
-                             const int32_t* __restrict__ perm, double* __restrict__ src,
-                             double* __restrict__ src_box) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= Npad) return;  // Npad is a multiple of 32 and blockDim: whole warps exit together
+__device__ __forceinline__ void pack_source_at(int64_t i, const double* __restrict__ xyz,
+                                               const double* __restrict__ nrm, const double* __restrict__ wgt,
+                                               const double* __restrict__ f, const double* __restrict__ q,
+                                               int64_t N, int64_t Npad, const int32_t* __restrict__ perm,
+                                               double* __restrict__ src, double* __restrict__ src_box) {
+  if (i >= Npad) return;  // Npad is a multiple of 32 and of the block size: whole warps exit together
   const bool pad = i >= N;
   const int64_t j = perm[pad ? N - 1 : i];
   const double w = pad ? 0.0 : wgt[j];
@@ -247,16 +321,26 @@ __global__ void pack_sources(const double* __restrict__ xyz, const double* __res
   }
 }
 
+template <int MODE>
+__global__ void pack_sources(const double* __restrict__ xyz, const double* __restrict__ nrm,
+                             const double* __restrict__ wgt, const double* __restrict__ f,
+                             const double* __restrict__ q, int64_t N, int64_t Npad,
+                             const int32_t* __restrict__ perm, double* __restrict__ src,
+                             double* __restrict__ src_box) {
+  pack_source_at<MODE>(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, xyz, nrm, wgt, f, q, N, Npad, perm, src,
+                       src_box);
+}
+
 struct Delta3 {
   double rho[3];
 };
 
 template <int MODE>
-__global__ void pack_targets(const double* __restrict__ xyz, const double* __restrict__ tb,
-                             const double* __restrict__ x0d, int64_t M, int64_t Mpad,
-                             const int32_t* __restrict__ perm, double h, Delta3 rho, bool sharp,
-                             double* __restrict__ tgt, int32_t* __restrict__ orig) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__device__ __forceinline__ void pack_target_at(int64_t i, const double* __restrict__ xyz,
+                                               const double* __restrict__ tb, const double* __restrict__ x0d,
+                                               int64_t M, int64_t Mpad, const int32_t* __restrict__ perm, double h,
+                                               const Delta3& rho, bool sharp, double* __restrict__ tgt,
+                                               int32_t* __restrict__ orig) {
   if (i >= Mpad) return;
   const int64_t j = perm[i < M ? i : M - 1];
   const double b = tb[j];
@@ -284,6 +368,32 @@ __global__ void pack_targets(const double* __restrict__ xyz, const double* __res
   tgt[F_W1 * Mpad + i] = w[1];
   tgt[F_W2 * Mpad + i] = w[2];
   orig[i] = static_cast<int32_t>(i < M ? j : -1);
+}
+
+template <int MODE>
+__global__ void pack_targets(const double* __restrict__ xyz, const double* __restrict__ tb,
+                             const double* __restrict__ x0d, int64_t M, int64_t Mpad,
+                             const int32_t* __restrict__ perm, double h, Delta3 rho, bool sharp,
+                             double* __restrict__ tgt, int32_t* __restrict__ orig) {
+  pack_target_at<MODE>(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, xyz, tb, x0d, M, Mpad, perm, h, rho, sharp,
+                       tgt, orig);
+}
+
+// Small problems: both packs in one launch (128-thread blocks: the first Npad/128 pack sources).
+template <int MODE>
+__global__ void pack_both(const double* __restrict__ sxyz, const double* __restrict__ nrm,
+                          const double* __restrict__ wgt, const double* __restrict__ f, const double* __restrict__ q,
+                          int64_t N, int64_t Npad, const int32_t* __restrict__ sperm, double* __restrict__ src,
+                          double* __restrict__ src_box, const double* __restrict__ txyz, const double* __restrict__ tb,
+                          const double* __restrict__ x0d, int64_t M, int64_t Mpad, const int32_t* __restrict__ tperm,
+                          double h, Delta3 rho, bool sharp, double* __restrict__ tgt, int32_t* __restrict__ orig) {
+  const int64_t sblocks = Npad / blockDim.x;
+  if (blockIdx.x < sblocks)
+    pack_source_at<MODE>(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, sxyz, nrm, wgt, f, q, N, Npad, sperm, src,
+                         src_box);
+  else
+    pack_target_at<MODE>((blockIdx.x - sblocks) * (int64_t)blockDim.x + threadIdx.x, txyz, tb, x0d, M, Mpad, tperm,
+                         h, rho, sharp, tgt, orig);
 }
 
 // ------------------------------------------------------------ K1: pair sums

@@ -200,6 +200,9 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override, int ph
   return p;
 }
 
+// N, M small enough for the one-CTA sort prologue (small_sort_kernel, kernels.cuh)
+bool small_problem(int64_t M, int64_t N) { return N <= kSmallSort && M <= kSmallSort; }
+
 bool rho_ok(const double* rho) {
   return rho && std::isfinite(rho[0]) && std::isfinite(rho[2]) && rho[0] > 0.0 && rho[1] > rho[0] &&
          rho[2] > rho[1];
@@ -283,24 +286,36 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   double* near_out = reinterpret_cast<double*>(ws + P.off_near);
   int* counter = reinterpret_cast<int*>(ws + P.off_counter);
 
-  if (cudaMemsetAsync(box, 0x7f, 3 * sizeof(long long), s) != cudaSuccess ||
-      cudaMemsetAsync(box + 3, 0x80, 3 * sizeof(long long), s) != cudaSuccess)
-    return STOKES_ER_ECUDA;
-  bbox_kernel<<<static_cast<int>(std::min<int64_t>(2 * 148, ceil_div(N + M, 256))), 256, 0, s>>>(sx, N, ty, M, box);
-  morton_kernel<<<ceil_div(N, 256), 256, 0, s>>>(sx, N, box, skin, svin);
-  morton_kernel<<<ceil_div(M, 256), 256, 0, s>>>(ty, M, box, tkin, tvin);
-  size_t cb = P.cub_bytes;
-  if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, skin, skout, svin, svout, (int)N, 0, 30, s) !=
-      cudaSuccess)
-    return STOKES_ER_ECUDA;
-  cb = P.cub_bytes;
-  if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, tkin, tkout, tvin, tvout, (int)M, 0, 30, s) !=
-      cudaSuccess)
-    return STOKES_ER_ECUDA;
-  pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox);
   Delta3 r3{{rho[0], rho[1], rho[2]}};
-  pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt,
-                                                            orig);
+  if (small_problem(M, N)) {
+    // small problems: box, keys and both sorts in one CTA, both packs in one launch (the same
+    // Morton order and records as below, 2 launches instead of ~15)
+    if (cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSortSmem) !=
+        cudaSuccess)
+      return STOKES_ER_ECUDA;
+    small_sort_kernel<<<1, kSmallSortThreads, kSmallSortSmem, s>>>(sx, N, ty, M, svout, tvout);
+    pack_both<MODE><<<static_cast<int>(P.Npad / kTile + ceil_div(P.Mpad, kTile)), kTile, 0, s>>>(
+        sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox, ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt, orig);
+  } else {
+    if (cudaMemsetAsync(box, 0x7f, 3 * sizeof(long long), s) != cudaSuccess ||
+        cudaMemsetAsync(box + 3, 0x80, 3 * sizeof(long long), s) != cudaSuccess)
+      return STOKES_ER_ECUDA;
+    bbox_kernel<<<static_cast<int>(std::min<int64_t>(2 * 148, ceil_div(N + M, 256))), 256, 0, s>>>(sx, N, ty, M,
+                                                                                                    box);
+    morton_kernel<<<ceil_div(N, 256), 256, 0, s>>>(sx, N, box, skin, svin);
+    morton_kernel<<<ceil_div(M, 256), 256, 0, s>>>(ty, M, box, tkin, tvin);
+    size_t cb = P.cub_bytes;
+    if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, skin, skout, svin, svout, (int)N, 0, 30, s) !=
+        cudaSuccess)
+      return STOKES_ER_ECUDA;
+    cb = P.cub_bytes;
+    if (cub::DeviceRadixSort::SortPairs(ws + P.off_cub, cb, tkin, tkout, tvin, tvout, (int)M, 0, 30, s) !=
+        cudaSuccess)
+      return STOKES_ER_ECUDA;
+    pack_sources<MODE><<<P.Npad / kTile, kTile, 0, s>>>(sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox);
+    pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt,
+                                                              orig);
+  }
   if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
 
   PairParams pp;
@@ -992,12 +1007,13 @@ int stokes_er_nodes_launch_count(int64_t N, int mode) {
 }
 
 int stokes_er_launch_count(int64_t M, int64_t N, int mode) {
-  (void)N;
   (void)mode;
   // bbox, 2x morton, pack sources, pack targets, fused far+near, finalize: our
   // kernels (default schedule; STOKES_ER_SCHEDULE_SEPARATE adds one).  The two
-  // CUB radix sorts add their own launches (library code).
-  return M > 0 ? 7 : 0;
+  // CUB radix sorts add their own launches (library code).  Small problems (N, M <=
+  // 16384): small_sort, pack_both, fused far+near, finalize (no CUB launches).
+  if (M <= 0) return 0;
+  return small_problem(M, N) ? 4 : 7;
 }
 
 const char* stokes_er_status_string(int status) {
