@@ -718,6 +718,14 @@ def sharded_step(arrs, block, evaluate_fn):
     return sharding.evaluate_sharded(*arrs, block.h, block.rho, mode=3, gather=True, evaluate_fn=evaluate_fn)
 
 
+def nodes_sharded_step(src_arrs, block, opt, ws, stream):
+    """The multi-rank node-path step: shard `rank` of the symmetric evaluation, then the all-reduce
+    of u, v (sharding.evaluate_nodes_sharded)."""
+    from paper_2507_00156_b200 import sharding
+    return sharding.evaluate_nodes_sharded(*src_arrs, block.h, block.rho, mode=3, options=opt, workspace=ws,
+                                           stream=stream)
+
+
 def run_eval(args, rank, world):
     """The default bench: one step = one full SL+DL 3-delta evaluation of BASELINE.json
     config --config at 1/h = --inv-h (default config 5 at 1/h = 256: the unit sphere's
@@ -764,9 +772,9 @@ def run_eval(args, rank, world):
     L = ser._lib.load()
     # auto: the node path for config 5 on one GPU from N ~ 1.5e5 on (below that the general path is faster:
     # 1/h = 64: 17.8 vs 15.9 ms; 1/h = 128: 204 vs 211 ms; 1/h = 256: 2.93 vs 3.25 s)
-    nodes = args.path == "nodes" or (args.path == "auto" and args.config == 5 and world == 1 and N >= 150000)
-    if nodes and (world > 1 or args.config != 5):
-        raise SystemExit("--path nodes: node-target workloads (config 5) on one GPU")
+    nodes = args.path == "nodes" or (args.path == "auto" and args.config == 5 and N >= 150000)
+    if nodes and args.config != 5:
+        raise SystemExit("--path nodes: node-target workloads (config 5)")
     if nodes:
         ws = torch.empty(ser.nodes_workspace_bytes(N, 3, opt), dtype=torch.uint8, device=dev)
     else:
@@ -792,6 +800,8 @@ def run_eval(args, rank, world):
             opt.pair_kernel_end_event = ev_pair[1].cuda_event if ev_pair else None
             opt.near_kernel_start_event = ev_near[0].cuda_event if ev_near else None
             opt.near_kernel_end_event = ev_near[1].cuda_event if ev_near else None
+            if world > 1:  # shard r of the block-pair items + one all-reduce of u, v
+                return nodes_sharded_step(arrs[:5], block, opt, ws, stream)
             ser.evaluate_nodes(*arrs[:5], block.h, block.rho, out_u=out_u, out_v=out_v, workspace=ws, stream=stream,
                                options=opt)
             return out_u, out_v
@@ -840,7 +850,15 @@ def run_eval(args, rank, world):
         host = [torch.from_numpy(a).pin_memory() for a in block.arrays()]
         hu = torch.empty((3, M), dtype=torch.float64).pin_memory()
         hv = torch.empty((3, M), dtype=torch.float64).pin_memory()
-        if nodes:
+        if nodes and world > 1:
+            host = host[:5]  # the targets are the nodes: only the source arrays travel
+
+            def e_step():
+                d = [t.to(dev, non_blocking=True) for t in host]
+                uu, vv = nodes_sharded_step(d, block, opt, ws, stream)
+                hu.copy_(uu, non_blocking=True)
+                hv.copy_(vv, non_blocking=True)
+        elif nodes:
             host = host[:5]  # the targets are the nodes: only the source arrays travel
             hws = torch.empty(int(L.stokes_er_nodes_host_workspace_bytes(N, 3)), dtype=torch.uint8, device=dev)
             e_step = lambda: ser.evaluate_nodes_host(*host, block.h, block.rho, out_u=hu, out_v=hv, workspace=hws,
@@ -875,7 +893,9 @@ def run_eval(args, rank, world):
         e2e = {"value": pairs * ke / e_total, "unit": UNIT,
                "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in host)),
                "d2h_bytes_per_step": int(hu.numel() * 8 + hv.numel() * 8),
-               "api": ("stokes_er_eval_nodes_host (C ABI, pinned host buffers)" if nodes else
+               "api": ("host->device copies + sharding.evaluate_nodes_sharded (all-reduce) + device->host copy"
+                       if nodes and world > 1 else
+                       "stokes_er_eval_nodes_host (C ABI, pinned host buffers)" if nodes else
                        "stokes_er_eval_host (C ABI, pinned host buffers)" if world == 1 else
                        "host->device copies + sharding.evaluate_sharded (all-gather) + device->host copy")}
 
@@ -889,8 +909,9 @@ def run_eval(args, rank, world):
     clocks = clk.summary()
     far_avg_s = statistics.mean(pair_ms) / 1e3
     far = pairs - near
-    # per-rank kernel work: the local target range's share (Morton ranges: near pairs ~ uniform)
-    share = M_loc / M
+    # per-rank kernel work: the local target range's share (Morton ranges: near pairs ~ uniform), or the
+    # rank's 1/world of the node path's block-pair items
+    share = (1.0 / world) if nodes else M_loc / M
     f_clk = 1965.0
     peak = SMS * FP64_LANES_PER_SM * 2 * f_clk * 1e6 / 1e12  # TFLOP/s
     peak_source = ("derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz max SM clock (MEASURED_PEAKS.json has "
@@ -899,8 +920,8 @@ def run_eval(args, rank, world):
     if nodes:
         sym_pairs, nbr_pairs = ser.nodes_pair_counts(N, block.h, block.rho, ws, stream=stream)
     if nodes:
-        k_flops = sym_pairs / 2 * F_SYM_UNORDERED_ALG
-        k_issued = sym_pairs / 2 * F_SYM_UNORDERED_ISSUED
+        k_flops = sym_pairs / 2 * F_SYM_UNORDERED_ALG * share
+        k_issued = sym_pairs / 2 * F_SYM_UNORDERED_ISSUED * share
         kname = ("sym_kernel<3> (FP64 pipe): the far-field sum (PAPER.md:183-191) over all-far 64-node block "
                  "pairs, one evaluation of each pair's shared part for both directed pairs (node targets)")
         kprefix = "void ser::sym_kernel<3>"
@@ -939,8 +960,8 @@ def run_eval(args, rank, world):
     near_info = None
     if nodes:
         near_avg_s = statistics.mean(near_ms) / 1e3
-        roofline["far_pairs_per_s"] = sym_pairs / far_avg_s
-        roofline["frac_57_flop_convention"] = sym_pairs * F_FAR_ALG / far_avg_s / 1e12 / peak
+        roofline["far_pairs_per_s"] = sym_pairs * share / far_avg_s
+        roofline["frac_57_flop_convention"] = sym_pairs * share * F_FAR_ALG / far_avg_s / 1e12 / peak
         roofline["directed_pairs"] = sym_pairs
         nbr_far = nbr_pairs - near
         near_info = {"kernel": "nbr_kernel<3>: near 3-delta pairs + the far pairs of the block pairs the "
@@ -971,6 +992,9 @@ def run_eval(args, rank, world):
                        "schedule": "nodes" if nodes else args.schedule,
                        "path": "stokes_er_eval_nodes" if nodes else "stokes_er_eval",
                        "parallelism": ("single GPU" if world == 1 else
+                                       f"node-path shards x{world}: 1/{world} of the symmetric kernel's block-pair "
+                                       "items and of the neighbour units per rank (sharding.evaluate_nodes_sharded), "
+                                       "all-reduce of u, v in the timed region" if nodes else
                                        f"target-sharded x{world}: Morton ranges of ONE target set "
                                        "(sharding.evaluate_sharded), sources replicated, all-gather of u, v in the "
                                        "timed region")},

@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define STOKES_ER_ABI_VERSION 3  /* 3: node-target entry points (stokes_er_eval_nodes*); 2: options.schedule, NEXT-2, NEXT-3 */
+#define STOKES_ER_ABI_VERSION 4  /* 4: options.shard_index/shard_count; 3: node-target entry points; 2: options.schedule, NEXT-2, NEXT-3 */
 /* c: near iff r <= c * max(delta_k)  ("s1=s2=s3=1 for t > 6") */
 #define STOKES_ER_CUTOFF 6.0
 /* c for the on-surface s# variant: 1 - s2#(6) = 2.45e-12, 1 - s_i#(7) < 1e-16 (R15) */
@@ -153,7 +153,7 @@ int stokes_er_eval_onsurface(const double* src_xyz, const double* src_normal, co
                              double* out_u, double* out_v, void* workspace, size_t workspace_bytes,
                              void* stream);
 
-/* Number of kernel launches one stokes_er_eval(M, N, mode) enqueues (ours; 4 when N, M <= 16384: the
+/* Number of kernel launches one stokes_er_eval(M, N, mode) enqueues (ours; 4 when N, M <= 8192: the
  * one-CTA sort prologue; 7 otherwise, plus the CUB radix-sort launches). */
 int stokes_er_launch_count(int64_t M, int64_t N, int mode);
 
@@ -177,6 +177,12 @@ typedef struct {
                                     Both give the same sums (same per-slot partials, same fixed-order
                                     finalize).  FUSED records only the pair_kernel events (around
                                     the one pair kernel). */
+  int shard_index;               /* node path (stokes_er_eval_nodes_ex) only: with shard_count > 1 this call */
+  int shard_count;               /* computes shard shard_index of the evaluation -- a contiguous 1/shard_count
+                                    of the symmetric kernel's block-pair items and of the neighbour units'
+                                    target groups -- and returns PARTIAL out_u, out_v (chi q0 only in shard
+                                    0) whose sum over the shards is the evaluation (one all-reduce across
+                                    GPUs).  0 / 0 or 0 / 1: the whole evaluation. */
 } stokes_er_options;
 
 #define STOKES_ER_SCHEDULE_FUSED 0

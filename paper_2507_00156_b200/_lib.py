@@ -28,7 +28,7 @@ class Options(ctypes.Structure):
                 ("targets_per_thread", ctypes.c_int), ("source_chunk_tiles", ctypes.c_int),
                 ("stats", ctypes.c_int64 * 4), ("near_kernel_start_event", ctypes.c_void_p),
                 ("near_kernel_end_event", ctypes.c_void_p), ("near_phases", ctypes.c_int),
-                ("schedule", ctypes.c_int)]
+                ("schedule", ctypes.c_int), ("shard_index", ctypes.c_int), ("shard_count", ctypes.c_int)]
 
 
 class Drop(ctypes.Structure):

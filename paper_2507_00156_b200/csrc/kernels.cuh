@@ -208,10 +208,10 @@ __global__ void morton_kernel(const double* __restrict__ x, int64_t n, const lon
   vals[i] = static_cast<int32_t>(i);
 }
 
-// Small problems (N, M <= kSmallSort): bounding box, Morton keys and a stable radix sort of
-// sources and of targets in ONE CTA (the same keys and the same stable order as bbox_kernel +
-// morton_kernel + the CUB device sorts, so the same sums), instead of ~15 launches.
-constexpr int kSmallSortThreads = 1024, kSmallSortItems = 16;
+// Small problems (N, M <= kSmallSort): bounding box, Morton keys and a stable radix sort of the
+// sources (CTA 0) and of the targets (CTA 1) in ONE launch (the same keys and the same stable
+// order as bbox_kernel + morton_kernel + the CUB device sorts, so the same sums), instead of ~15.
+constexpr int kSmallSortThreads = 1024, kSmallSortItems = 8;
 constexpr int64_t kSmallSort = (int64_t)kSmallSortThreads * kSmallSortItems;
 constexpr int kSmallSortSmem =
     (int)sizeof(typename cub::BlockRadixSort<uint32_t, kSmallSortThreads, kSmallSortItems, int32_t>::TempStorage);
@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(kSmallSortThreads, 1) small_sort_kernel(const 
       bhi[d] = fmax(bhi[d], red[k][3 + d]);
     }
   }
-  for (int pass = 0; pass < 2; ++pass) {
+  {
+    const int pass = blockIdx.x;  // CTA 0 sorts the sources, CTA 1 the targets (both computed the same box)
     const double* x = pass == 0 ? sx : tx;
     const int64_t n = pass == 0 ? N : M;
     int32_t* out = pass == 0 ? svout : tvout;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kSmallSortThreads, 1) small_sort_kernel(const 
       keys[k] = i < n ? morton_key(x, n, i, blo, bhi) : 0x3fffffffu;  // padding sorts last (stable)
       vals[k] = static_cast<int32_t>(i);
     }
-    __syncthreads();  // tmp free
+    __syncthreads();  // red read by every thread before tmp (may alias nothing, but keep the order simple)
     Sort(tmp).Sort(keys, vals, 0, 30);
 #pragma unroll
     for (int k = 0; k < kSmallSortItems; ++k) {
@@ -989,6 +990,44 @@ __global__ void __launch_bounds__(kThreads, SER_FAR_MINB) fused_kernel(const Pai
 }
 
 // ------------------------------------------------------------ K2: finalize
+// Small M (many partial slots per target: fine far chunks, up to 64 near phases): one warp per
+// target, lanes stride over the slots, a fixed butterfly combines them (deterministic).
+template <int MODE>
+__global__ void finalize_small_kernel(const double* __restrict__ partial, const double* __restrict__ near_out,
+                                      const double* __restrict__ tgt, const int32_t* __restrict__ orig, int64_t M,
+                                      int64_t Mpad, int n_chunks, int TB, int phases, double* __restrict__ out_u,
+                                      double* __restrict__ out_v) {
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= M) return;  // whole warps
+  const int64_t tb = i / TB, loc = i - tb * TB;
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  for (int ch = lane; ch < n_chunks; ch += 32) {
+    const double* pp = partial + ((tb * n_chunks + ch) * 6) * TB + loc;
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+      if ((c < 3 && (MODE & 1)) || (c >= 3 && (MODE & 2))) s[c] += pp[c * TB];
+  }
+  for (int ph = lane; ph < phases; ph += 32)
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+      if ((c < 3 && (MODE & 1)) || (c >= 3 && (MODE & 2))) s[c] += near_out[((int64_t)ph * 6 + c) * Mpad + i];
+#pragma unroll
+  for (int c = 0; c < 6; ++c)
+    for (int o = 16; o; o >>= 1) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
+  if (lane != 0) return;
+  const int64_t o = orig[i];
+  const double inv8pi = 1.0 / (8.0 * kPi);
+  if (MODE & 1)
+    for (int c = 0; c < 3; ++c) out_u[c * M + o] = s[c] * inv8pi;                 // eq. (10)
+  if (MODE & 2) {
+    const double b = tgt[(int64_t)F_B * Mpad + i];
+    const double chi = b < 0.0 ? 1.0 : (b > 0.0 ? 0.0 : 0.5);
+    for (int c = 0; c < 3; ++c)                                                  // eq. (11), T = -6...
+      out_v[c * M + o] = -6.0 * s[3 + c] * inv8pi + chi * tgt[(F_Q0 + c) * Mpad + i];
+  }
+}
+
 template <int MODE>
 __global__ void finalize_kernel(const double* __restrict__ partial, const double* __restrict__ near_out,
                                 const double* __restrict__ tgt, const int32_t* __restrict__ orig, int64_t M,

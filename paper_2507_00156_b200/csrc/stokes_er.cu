@@ -293,7 +293,7 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
     if (cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSortSmem) !=
         cudaSuccess)
       return STOKES_ER_ECUDA;
-    small_sort_kernel<<<1, kSmallSortThreads, kSmallSortSmem, s>>>(sx, N, ty, M, svout, tvout);
+    small_sort_kernel<<<2, kSmallSortThreads, kSmallSortSmem, s>>>(sx, N, ty, M, svout, tvout);
     pack_both<MODE><<<static_cast<int>(P.Npad / kTile + ceil_div(P.Mpad, kTile)), kTile, 0, s>>>(
         sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox, ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt, orig);
   } else {
@@ -387,8 +387,13 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
     opt->stats[2] = P.chunk_tiles;
     opt->stats[3] = P.T;
   }
-  finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad, P.n_chunks,
-                                                          kThreads * P.T, P.near_phases, out_u, out_v);
+  if (small_problem(M, N))  // many slots per target, few targets: a warp per target
+    finalize_small_kernel<MODE><<<ceil_div(M * 32, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad,
+                                                                      P.n_chunks, kThreads * P.T, P.near_phases,
+                                                                      out_u, out_v);
+  else
+    finalize_kernel<MODE><<<ceil_div(M, 256), 256, 0, s>>>(partial, near_out, tgt, orig, M, P.Mpad, P.n_chunks,
+                                                            kThreads * P.T, P.near_phases, out_u, out_v);
   return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
 }
 
@@ -644,6 +649,9 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
   if (cudaMemsetAsync(pacc, 0, (size_t)P.G * 6 * P.Npad * sizeof(double), s) != cudaSuccess ||
       cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess)
     return STOKES_ER_ECUDA;
+  if (opt && opt->shard_count > 1 &&  // a shard writes only its groups' neighbour partials: zero the rest
+      cudaMemsetAsync(near_out, 0, (size_t)P.near_phases * P.Npad * 6 * sizeof(double), s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
   const double dmax = rho[2] * h;
   const double cutoff = SHARP ? STOKES_ER_CUTOFF_SURFACE : STOKES_ER_CUTOFF;
   const double rc2 = (cutoff * dmax) * (cutoff * dmax);
@@ -657,6 +665,12 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
   sp.chunk = P.chunk;
   sp.nchunks = P.nchunks;
   sp.n_items = P.n_items;
+  // a shard (options.shard_index / shard_count) takes a contiguous share of the items and of the
+  // neighbour units' target groups, and returns partial sums
+  const int nshard = (opt && opt->shard_count > 1) ? opt->shard_count : 1;
+  const int ishard = nshard > 1 ? opt->shard_index : 0;
+  sp.item_begin = P.n_items * ishard / nshard;
+  sp.item_end = P.n_items * (ishard + 1) / nshard;
   sp.rc2_box = rc2 * (1.0 + 1e-9);
   NearParams np;
   np.src = src;
@@ -665,7 +679,10 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
   np.near_out = near_out;
   np.counter = counter + 1;
   np.phases = P.near_phases;
-  np.n_units = static_cast<int>((P.Npad / 32) * P.near_phases);
+  const int64_t n_groups = P.Npad / 32;
+  const int64_t g0 = n_groups * ishard / nshard, g1 = n_groups * (ishard + 1) / nshard;
+  const int unit_base = static_cast<int>(g0 * P.near_phases);
+  np.n_units = static_cast<int>((g1 - g0) * P.near_phases);
   np.Mpad = P.Npad;
   np.Npad = P.Npad;
   np.rc2 = rc2;
@@ -685,7 +702,7 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbr_kernel<MODE, SHARP>, 64, 0);
     const int ngrid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(np.n_units, 2), (int64_t)sms * std::max(occ, 1))));
-    nbr_kernel<MODE, SHARP><<<ngrid, 64, 0, s>>>(np, blkbox);
+    nbr_kernel<MODE, SHARP><<<ngrid, 64, 0, s>>>(np, blkbox, unit_base);
   }
   if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
   if (opt) {
@@ -695,7 +712,7 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
     opt->stats[3] = 2;
   }
   finalize_nodes<MODE><<<ceil_div(N, 256), 256, 0, s>>>(pacc, P.G, near_out, P.near_phases, tgt, orig, N, P.Npad,
-                                                         out_u, out_v);
+                                                         ishard == 0 ? 0.5 : 0.0, out_u, out_v);
   return cudaGetLastError() == cudaSuccess ? STOKES_ER_OK : STOKES_ER_ECUDA;
 }
 
@@ -899,6 +916,9 @@ int stokes_er_eval_nodes_ex(const double* src_xyz, const double* src_normal, con
   if (st) return st;
   if (((mode & 1) && !out_u) || ((mode & 2) && !out_v)) return STOKES_ER_EINVAL;
   if ((st = check_arch())) return st;
+  if (options && options->shard_count > 1 &&
+      (options->shard_index < 0 || options->shard_index >= options->shard_count))
+    return STOKES_ER_EINVAL;
   const NodePlan P = make_node_plan(N, mode, opt_phases(options));
   if (!workspace || workspace_bytes < P.total) return STOKES_ER_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1011,7 +1031,7 @@ int stokes_er_launch_count(int64_t M, int64_t N, int mode) {
   // bbox, 2x morton, pack sources, pack targets, fused far+near, finalize: our
   // kernels (default schedule; STOKES_ER_SCHEDULE_SEPARATE adds one).  The two
   // CUB radix sorts add their own launches (library code).  Small problems (N, M <=
-  // 16384): small_sort, pack_both, fused far+near, finalize (no CUB launches).
+  // 8192): small_sort, pack_both, fused far+near, finalize (no CUB launches).
   if (M <= 0) return 0;
   return small_problem(M, N) ? 4 : 7;
 }

@@ -17,7 +17,8 @@
 //                      block or of a block that is not AF: far pairs (masked)
 //                      and the near 3-delta pairs (the near unit's queue)
 //   finalize_nodes     K7: sums the per-CTA accumulators (fixed order) and the
-//                      K6 partials, applies 1/(8 pi), -6 and chi q0 = q/2
+//                      K6 partials, applies 1/(8 pi), -6 and chi q0 = q/2 (b = 0; a shard other
+//                      than 0 of a sharded call adds no chi term: the shards' sum has it once)
 //
 // Determinism: sym_kernel assigns items to CTAs statically (item i -> CTA
 // i mod G) and every CTA accumulates into its OWN slice of the workspace, in
@@ -69,6 +70,7 @@ struct SymParams {
   int chunk;              // R blocks per item (a multiple of kSymWarps)
   int nchunks;
   int64_t n_items;
+  int64_t item_begin, item_end;  // this call's items (a shard of [0, n_items), or all of them)
   double rc2_box;
 };
 
@@ -289,7 +291,9 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
   uint32_t phase_bits = 0;
   double* my_acc = p.pacc + (int64_t)blockIdx.x * 6 * p.Npad;
   // this CTA's contiguous range of the c-major item list (static: deterministic sums)
-  const int64_t item_lo = (int64_t)blockIdx.x * p.n_items / G, item_hi = ((int64_t)blockIdx.x + 1) * p.n_items / G;
+  const int64_t n_mine = p.item_end - p.item_begin;
+  const int64_t item_lo = p.item_begin + (int64_t)blockIdx.x * n_mine / G;
+  const int64_t item_hi = p.item_begin + ((int64_t)blockIdx.x + 1) * n_mine / G;
   int cur_c = -1;
   auto flush_chunk = [&](int c) {  // the chunk's R sums into this CTA's slice
     const int r0 = c * p.chunk, nr = min(p.chunk, p.nb - r0);
@@ -558,7 +562,8 @@ __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __re
 }
 
 template <int MODE, bool SHARP>
-__global__ void __launch_bounds__(64, 6) nbr_kernel(const NearParams p, const double* __restrict__ blk_box) {
+__global__ void __launch_bounds__(64, 6) nbr_kernel(const NearParams p, const double* __restrict__ blk_box,
+                                                    int unit_base) {
   __shared__ NbrSmem s_nb[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
@@ -566,7 +571,7 @@ __global__ void __launch_bounds__(64, 6) nbr_kernel(const NearParams p, const do
     if (lane == 0) unit = atomicAdd(p.counter, 1);
     unit = __shfl_sync(0xffffffffu, unit, 0);
     if (unit >= p.n_units) break;
-    nbr_unit<MODE, SHARP>(p, blk_box, unit, s_nb[warp]);
+    nbr_unit<MODE, SHARP>(p, blk_box, unit_base + unit, s_nb[warp]);  // this call's units: [base, base + n)
   }
 }
 
@@ -589,7 +594,8 @@ __global__ void sym_pair_count(const double* __restrict__ blk_box, int nb, int64
 template <int MODE>
 __global__ void finalize_nodes(const double* __restrict__ pacc, int G, const double* __restrict__ near_out,
                                int phases, const double* __restrict__ tgt, const int32_t* __restrict__ orig,
-                               int64_t N, int64_t Npad, double* __restrict__ out_u, double* __restrict__ out_v) {
+                               int64_t N, int64_t Npad, double chi, double* __restrict__ out_u,
+                               double* __restrict__ out_v) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
   double s[6] = {0, 0, 0, 0, 0, 0};
@@ -607,7 +613,7 @@ __global__ void finalize_nodes(const double* __restrict__ pacc, int G, const dou
     for (int k = 0; k < 3; ++k) out_u[k * N + o] = s[k] * inv8pi;                            // eq. (10)
   if (MODE & 2)
     for (int k = 0; k < 3; ++k)                                                               // eq. (11), chi = 1/2
-      out_v[k * N + o] = -6.0 * s[3 + k] * inv8pi + 0.5 * tgt[(F_Q0 + k) * Npad + i];
+      out_v[k * N + o] = -6.0 * s[3 + k] * inv8pi + chi * tgt[(F_Q0 + k) * Npad + i];
 }
 
 }  // namespace ser

@@ -1,10 +1,11 @@
-"""Multi-GPU target sharding.
+"""Multi-GPU sharding.
 
-Targets are independent (the paper's own parallelism is a
-loop over targets), so one process per GPU evaluates a contiguous range of
-the targets against all sources.  There is no data-path collective; the only
-collectives are an optional all-gather of the outputs and the max-over-ranks
-timing reduction of bench.py.
+General targets are independent (the paper's own parallelism
+is a loop over targets), so one process per GPU evaluates a contiguous range
+of the Morton-sorted targets against all sources, and an optional all-gather
+assembles the field (evaluate_sharded).  Node targets (evaluate_nodes_sharded)
+split the symmetric kernel's block-pair items instead, and one all-reduce sums
+the ranks' partial fields.  bench.py adds a max-over-ranks timing reduction.
 """
 from __future__ import annotations
 
@@ -117,3 +118,35 @@ def evaluate_sharded(src_xyz, src_normal, src_weight, f, q, tgt_xyz, tgt_b, tgt_
         return out
 
     return full(u), full(v)
+
+
+def evaluate_nodes_sharded(src_xyz, src_normal, src_weight, f, q, h, rho, mode=3, group=None,
+                           evaluate_fn: Optional[Callable] = None, options=None, workspace=None, stream=None):
+    """The node-target evaluation (stokes_er_eval_nodes) split across the ranks of `group`.
+
+    Node targets make the far sum symmetric: one block-pair item adds to the
+    nodes of BOTH blocks, so the work does not split by target ranges.  Rank r computes shard r
+    of the evaluation -- a contiguous 1/world of the symmetric kernel's items and of the
+    neighbour units' target groups (options.shard_index / shard_count) -- whose partial u, v
+    (chi q0 only on rank 0) sum over the ranks to the evaluation: ONE all-reduce (sum) of the
+    48 N bytes, the path's exchange step.  Every rank returns the full u, v.
+    `evaluate_fn(src_xyz, src_normal, src_weight, f, q, h, rho, mode, shard_index, shard_count)`
+    defaults to the CUDA path (paper_2507_00156_b200.evaluate_nodes)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if evaluate_fn is None:
+        from . import Options, evaluate_nodes
+
+        def evaluate_fn(sx, sn, sw, ff, qq, hh, rr, md, si, sc):
+            opt = options if options is not None else Options()
+            opt.shard_index, opt.shard_count = si, sc
+            return evaluate_nodes(sx, sn, sw, ff, qq, hh, rr, mode=md, workspace=workspace, stream=stream,
+                                  options=opt)
+    u, v = evaluate_fn(src_xyz, src_normal, src_weight, f, q, h, rho, mode, rank, world)
+    if world > 1:
+        for t in (u, v):
+            if t is not None:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return u, v

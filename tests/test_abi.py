@@ -39,7 +39,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_pure_host_queries(lib):
-    assert lib.stokes_er_abi_version() == 3
+    assert lib.stokes_er_abi_version() == 4
     assert lib.stokes_er_nodes_launch_count(0, 3) == 0 and lib.stokes_er_nodes_launch_count(10, 3) == 8
     assert lib.stokes_er_status_string(5) == b"GMRES reached max_iter above the tolerance"
     assert lib.stokes_er_status_string(3) == b"workspace too small"

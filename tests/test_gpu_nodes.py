@@ -250,3 +250,27 @@ def test_onsurface_sharp_at_nodes(ser, inv_h, mode):
         assert rel(u.cpu().numpy(), ug.cpu().numpy()) <= 1e-13
     if mode & 2:
         assert rel(v.cpu().numpy(), vg.cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("count", [2, 3])
+def test_shards_sum_to_the_evaluation(ser, count):
+    """options.shard_index / shard_count (the multi-GPU split of the node path, one all-reduce):
+    the shards' partial u, v, computed one after another on this GPU, sum to the evaluation."""
+    import torch
+
+    blk = config5(inv_h=32)
+    arrs = [torch.from_numpy(a).cuda() for a in (blk.src_xyz, blk.src_normal, blk.src_weight, blk.f, blk.q)]
+    u, v = ser.evaluate_nodes(*arrs, blk.h, blk.rho)
+    su = torch.zeros_like(u)
+    sv = torch.zeros_like(v)
+    for r in range(count):
+        o = ser.Options()
+        o.shard_index, o.shard_count = r, count
+        pu, pv = ser.evaluate_nodes(*arrs, blk.h, blk.rho, options=o)
+        su += pu
+        sv += pv
+    assert rel(su.cpu().numpy(), u.cpu().numpy()) <= 1e-13 and rel(sv.cpu().numpy(), v.cpu().numpy()) <= 1e-13
+    o = ser.Options()
+    o.shard_index, o.shard_count = count, count
+    with pytest.raises(ser.StokesERError):
+        ser.evaluate_nodes(*arrs, blk.h, blk.rho, options=o)

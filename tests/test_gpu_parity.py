@@ -451,9 +451,9 @@ def test_wide_rho_ratio(ser, rho):
     check_block(ser, blk, localized=False)
 
 
-@pytest.mark.parametrize("n", [16384, 16385])
+@pytest.mark.parametrize("n", [8192, 8193])
 def test_small_sort_prologue_boundary(ser, n):
-    """N, M <= 16384 take the one-CTA sort prologue (small_sort_kernel + pack_both), larger
+    """N, M <= 8192 take the one-launch sort prologue (small_sort_kernel + pack_both), larger
     problems bbox + morton + the CUB device sorts: both sides of the boundary against the oracle
     (the first n nodes of the 1/h = 32 sphere as sources, a target sample of config 2)."""
     import dataclasses
@@ -464,4 +464,4 @@ def test_small_sort_prologue_boundary(ser, n):
                               src_weight=cut(blk.src_weight), f=cut(blk.f), q=cut(blk.q))
     sub = sub.take_targets(np.arange(0, blk.M, 37))
     check_block(ser, sub, localized=True)
-    assert ser.launch_count(sub.M, n) == (4 if n <= 16384 else 7)
+    assert ser.launch_count(sub.M, n) == (4 if n <= 8192 else 7)

@@ -146,3 +146,57 @@ def test_bench_multirank_arm_goes_through_evaluate_sharded(tmp_path):
     u_ref, v_ref = oracle.evaluate_block(blk)
     np.testing.assert_array_equal(np.load(tmp_path / "bu.npy"), u_ref)
     np.testing.assert_array_equal(np.load(tmp_path / "bv.npy"), v_ref)
+
+
+def _nodes_worker(rank, world, port, out_dir):
+    """sharding.evaluate_nodes_sharded: each rank's partial (here a stand-in: the oracle over this
+    rank's share of the sources, chi q0 only on rank 0 -- the same linearity the CUDA shards use)
+    is all-reduced into the full field on every rank."""
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2507_00156_b200.sharding import evaluate_nodes_sharded, shard_bounds
+    from workloads.configs import config5, node_block
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    blk = node_block(config5(inv_h=8))
+    calls = []
+
+    def partial_fn(sx, sn, sw, f, q, h, rho, mode, si, sc):
+        calls.append((si, sc))
+        a, b = shard_bounds(blk.N, si, sc)
+        w = np.zeros(blk.N)
+        w[a:b] = blk.src_weight[a:b]  # this shard's sources (the rest weigh 0: add exactly 0)
+        u, v = oracle.evaluate(blk.src_xyz, blk.src_normal, w, blk.f, blk.q, blk.tgt_xyz, blk.tgt_b,
+                               blk.tgt_x0_density, h, rho, mode=mode, localized=True)
+        if si != 0:
+            v = v - 0.5 * blk.q  # chi q0 once, on shard 0
+        return torch.from_numpy(u), torch.from_numpy(v)
+
+    t = lambda a: torch.from_numpy(a)
+    u, v = evaluate_nodes_sharded(t(blk.src_xyz), t(blk.src_normal), t(blk.src_weight), t(blk.f), t(blk.q), blk.h,
+                                  blk.rho, evaluate_fn=partial_fn)
+    assert calls == [(rank, world)]
+    np.save(os.path.join(out_dir, f"nu{rank}.npy"), u.numpy())
+    np.save(os.path.join(out_dir, f"nv{rank}.npy"), v.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_nodes_allreduce(tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle
+    from workloads.configs import config5, node_block
+
+    oracle.build()
+    port = _free_port()
+    mp.spawn(_nodes_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    blk = node_block(config5(inv_h=8))
+    u_ref, v_ref = oracle.evaluate_block(blk, localized=True)
+    for r in range(2):  # every rank holds the full field
+        u, v = np.load(tmp_path / f"nu{r}.npy"), np.load(tmp_path / f"nv{r}.npy")
+        assert np.abs(u - u_ref).max() <= 1e-13 * np.abs(u_ref).max()
+        assert np.abs(v - v_ref).max() <= 1e-13 * np.abs(v_ref).max()
