@@ -103,20 +103,28 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(y, fma(e, e, e), y);
 }
 
-// Smoothing factors at t = r/delta for t >= 0.5:
-//   E = erf t = 1 - e^{-t^2} erfcx(t), erfcx as one degree-12 polynomial in
-//   v = 1/(2.5 + t) (tools/gen_sfactor_coeffs.py; |error of E| <= 2.1e-16 on [0.5, 6]);
-//   s2 = E - (2/sqrt pi) t e^{-t^2},  c23 = s2 - s3 = (2/sqrt pi)(2/3) t^3 e^{-t^2}.
-// Branch-free, no tables; for t < 0.5 it returns finite values the caller discards.
-__device__ __forceinline__ void sfactor_s(double t, double& E, double& s2, double& c23, double* e_out = nullptr) {
-  const double u = t * t;
-  const double e = exp_neg(u);  // any u >= 0 (exp_neg clamps its exponent)
-  if (e_out) *e_out = e;  // e^{-t^2}, for callers that need it too (the s# factors)
-  const double tc = fmin(t, 6.0);  // erfc(t > 6) < 2e-17: E rounds to 1 either way
-  const double x = fma(rcp_nr(kErfcxKappa + tc), kErfcxVA, kErfcxVB);
+// The two ingredients of the smoothing factors at t = r/delta for t >= 0.5:
+//   e = e^{-t^2} and P = erfcx(t) as ONE degree-12 polynomial in v = 1/(2.5 + t)
+//   (tools/gen_sfactor_coeffs.py; |error of 1 - e P| <= 2.2e-16 for every t >= 0.5: fitted on
+//   [0.5, 6], and past 6 the polynomial still follows erfcx while e < 2.3e-16 -- checked to t = 40),
+//   so erf t = 1 - e P with no table, no piece selection and no clamp; u = t^2 is returned too.
+// Branch-free; for t < 0.5 it returns finite values the caller discards.
+__device__ __forceinline__ void sfactor_eP(double t, double& e, double& P, double& u) {
+  u = t * t;
+  e = exp_neg(u);  // any u >= 0 (exp_neg clamps its exponent)
+  const double x = fma(rcp_nr(kErfcxKappa + t), kErfcxVA, kErfcxVB);
   double p = kErfcxV[kErfcxDeg];
 #pragma unroll
   for (int j = kErfcxDeg - 1; j >= 0; --j) p = fma(p, x, kErfcxV[j]);
+  P = p;
+}
+
+// Smoothing factors (eqs. (14)-(16)) at t >= 0.5 from sfactor_eP:
+//   E = erf t = 1 - e P,  s2 = E - (2/sqrt pi) t e,  c23 = s2 - s3 = (2/sqrt pi)(2/3) t^3 e.
+__device__ __forceinline__ void sfactor_s(double t, double& E, double& s2, double& c23, double* e_out = nullptr) {
+  double e, p, u;
+  sfactor_eP(t, e, p, u);
+  if (e_out) *e_out = e;  // e^{-t^2}, for callers that need it too (the s# factors)
   E = fma(-e, p, 1.0);
   const double gt = (kTwoOverSqrtPi * e) * t;
   s2 = E - gt;

@@ -716,15 +716,20 @@ __device__ __forceinline__ void near_pair(const Src& s, double y0, double y1, do
   }
   // all three deltas through the branch-free table path (independent chains)
   const double t0 = r * p.inv_delta[0], t1 = r * p.inv_delta[1], t2 = r * p.inv_delta[2];
-  double E0, E1, E2, s20, s21, s22, c0, c1, c2;
-  sfactor_s(t0, E0, s20, c0);
-  sfactor_s(t1, E1, s21, c1);
-  sfactor_s(t2, E2, s22, c2);
+  double e0, e1, e2, P0, P1, P2, u0, u1, u2;
+  sfactor_eP(t0, e0, P0, u0);
+  sfactor_eP(t1, e1, P1, u1);
+  sfactor_eP(t2, e2, P2, u2);
   const double tw0 = tf[NF_W0][lane], tw1 = tf[NF_W1][lane], tw2 = tf[NF_W2][lane];
   const double w0 = t0 >= 0.5 ? tw0 : 0.0, w1 = t1 >= 0.5 ? tw1 : 0.0, w2 = t2 >= 0.5 ? tw2 : 0.0;
-  const double S1 = fma(w0, E0, fma(w1, E1, w2 * E2));
-  const double S2 = fma(w0, s20, fma(w1, s21, w2 * s22));
-  const double C = fma(w0, c0, fma(w1, c1, w2 * c2));
+  // the weighted sums over k of w_k s_i(t_k) (eqs. (14)-(16)) with a_k = w_k e_k, b_k = a_k t_k:
+  //   S1 = sum w_k erf t_k = W - sum a_k P_k,  S2 = sum w_k s2 = S1 - (2/sqrt pi) sum b_k,
+  //   C = sum w_k (s2 - s3) = (2/sqrt pi)(2/3) sum b_k t_k^2,  W = sum w_k
+  const double a0 = w0 * e0, a1 = w1 * e1, a2 = w2 * e2;
+  const double S1 = fma(-a2, P2, fma(-a1, P1, fma(-a0, P0, (w0 + w1) + w2)));
+  const double b0 = a0 * t0, b1 = a1 * t1, b2 = a2 * t2;
+  const double S2 = fma(-kTwoOverSqrtPi, (b0 + b1) + b2, S1);
+  const double C = ((2.0 / 3.0) * kTwoOverSqrtPi) * fma(b2, u2, fma(b1, u1, b0 * u0));
   const double S3 = S2 - C;
   const double ri3 = ri * ri * ri;
   double A1 = S1 * ri, A3 = S2 * ri3, A5 = S3 * (ri3 * ri * ri), AP = C * ri3;
