@@ -45,7 +45,7 @@ F_NEAR_ALG = 180
 # s#1..3 polynomials 18, A1 A3 A5 5, SL 24, DL (unsplit, as the far pair) 21
 F_NEAR_SHARP_ALG = 84
 F_FAR_ISSUED = 64   # ncu-countable FP64 flops (2*DFMA + DMUL + DADD) of far_pair<3> (41 instructions)
-F_NEAR_ISSUED = 343  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r01/ncu_full_v15_far_near.json: 135 DFMA, 48 DMUL, 24 DADD)
+F_NEAR_ISSUED = 331  # ncu-counted FP64 flops per near pair of near_kernel<3> incl. its classification (profiles/r02/ncu_full_near_cfg2_h64.json: 132.3 DFMA, 41.1 DMUL, 25.5 DADD = 199 instructions; round 1: 343)
 # node-target path (csrc/sym.cuh): one evaluation of a far pair's shared part serves both directed
 # pairs.  Algorithmic flops per UNORDERED pair (rsqrt = 1, FMA = 2): d 3, r^2 5, rsqrt 1, 1/r^2 and
 # 1/r^5 3, SL 2 x 24, DL: q_j - q_i 3, d.dq 5, dq/r^5 1 shared + 2 x (d.mw 5, x 1, v += d c 6) = 93,
@@ -623,7 +623,7 @@ def committed_traffic(bench_cfg: dict, kernel_prefix: str):
                 for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     v, u = k[key].split()
                     tot += float(v.replace(",", "")) * units[u]
-                return int(tot), os.path.relpath(path, ROOT) + " (ncu --set full capture of this bench configuration)"
+                return int(tot), os.path.relpath(path, ROOT) + " (ncu capture of this bench configuration)"
     return None
 
 
