@@ -49,6 +49,9 @@ constexpr int kSymStages = 3;                              // R-block TMA ring
 #ifndef SER_SYM_PIPE
 #define SER_SYM_PIPE 0                                     // software-pipelined step (measured slower)
 #endif
+#ifndef SER_SYM_TR2
+#define SER_SYM_TR2 0                                      // 2 R nodes per step (4 pairs): tuning macro
+#endif
 #ifndef SER_SYM_UNROLL
 #define SER_SYM_UNROLL 4                                   // steps per loop iteration (2: -1%, 1: -1%)
 #endif
@@ -386,6 +389,28 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
           g0 = n0;
           g1 = n1;
         }
+#elif SER_SYM_TR2
+        // both halves at once: step kk pairs the lane's two I nodes with R node (lane + kk) & 31 of
+        // EACH half (4 independent pairs per step, two rotating accumulators)
+        Acc ra{0, 0, 0, 0, 0, 0}, rb{0, 0, 0, 0, 0, 0};
+        const double* Rb = R + kTileDoubles;
+#pragma unroll kSymUnroll
+        for (int kk = 0; kk < 32; ++kk) {
+          const SymNode rn = load_node<MODE>(R, (lane + kk) & 31);
+          const SymNode rm = load_node<MODE>(Rb, (lane + kk) & 31);
+          sym_pair<MODE>(I0, rn, a0, ra);
+          sym_pair<MODE>(I1, rn, a1, ra);
+          sym_pair<MODE>(I0, rm, a0, rb);
+          sym_pair<MODE>(I1, rm, a1, rb);
+          shfl_acc(ra, (lane + 1) & 31);
+          shfl_acc(rb, (lane + 1) & 31);
+        }
+        double* rw = red + warp * 6 * kBlk + lane;  // lane l holds R nodes l (ra) and 32 + l (rb)
+        rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
+        rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
+        rw += 32;
+        rw[0 * kBlk] = rb.u0; rw[1 * kBlk] = rb.u1; rw[2 * kBlk] = rb.u2;
+        rw[3 * kBlk] = rb.v0; rw[4 * kBlk] = rb.v1; rw[5 * kBlk] = rb.v2;
 #else
 #pragma unroll 1
         for (int hf = 0; hf < 2; ++hf) {
