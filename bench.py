@@ -335,12 +335,20 @@ def run_onsurface(args, rank, world):
     arrs = ser.to_device(block, dev)
     u = torch.empty((3, M), dtype=torch.float64, device=dev)
     v = torch.empty((3, M), dtype=torch.float64, device=dev)
-    ws = ser.alloc_workspace(M, N, 3, dev)
+    # every node is a target: the node path (symmetric far kernel) from 5e4 nodes on, as the two-drop
+    # self blocks; stokes_er_eval_onsurface below
+    nodes = args.path == "nodes" or (args.path == "auto" and N >= 50000)
+    if nodes:
+        ws = torch.empty(ser.nodes_workspace_bytes(N, 3), dtype=torch.uint8, device=dev)
+        run = lambda: ser.evaluate_nodes_onsurface(*arrs[:5], delta, out_u=u, out_v=v, workspace=ws)
+    else:
+        ws = ser.alloc_workspace(M, N, 3, dev)
+        run = lambda: ser.evaluate_onsurface(*arrs, delta, out_u=u, out_v=v, workspace=ws)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     K, W = args.steps, args.warmup
     for _ in range(W):
         flush.zero_()
-        ser.evaluate_onsurface(*arrs, delta, out_u=u, out_v=v, workspace=ws)
+        run()
     torch.cuda.synchronize(dev)
     ms = []
     with ClockSampler(local) as clk:
@@ -348,7 +356,7 @@ def run_onsurface(args, rank, world):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            ser.evaluate_onsurface(*arrs, delta, out_u=u, out_v=v, workspace=ws)
+            run()
             b.record()
             b.synchronize()
             ms.append(a.elapsed_time(b))
@@ -365,16 +373,21 @@ def run_onsurface(args, rank, world):
             "ms_per_step": 1e3 * total_s / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": block.name + "_onsurface", "N": N, "M": M, "delta_over_h": 3.0, "cutoff": 7.0,
+                       "path": "stokes_er_eval_nodes_onsurface" if nodes else "stokes_er_eval_onsurface",
                        "near_pairs_per_step": near, "l2": "flushed between timed steps (256 MiB write)",
                        "inputs": "resident in HBM"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel": f"the whole evaluation: {F_FAR_ALG} flops per far pair, {F_NEAR_SHARP_ALG} per "
-                                   "s# near pair (rsqrt, erf, exp = 1)",
+                                   "s# near pair (rsqrt, erf, exp = 1)" + (" -- counted per directed far pair; the "
+                                   "node path evaluates each pair's geometry once for both directions (46.5 "
+                                   "honest flops per directed pair, DESIGN.md 5.7)" if nodes else ""),
                          "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz"},
-            "clocks": clk.summary(), "gpu_launches": K * 7,
-            "gpu_launches_note": "per step: bbox, 2 morton, pack sources, pack targets, fused far+near, finalize "
-                                 "(+ CUB sort)",
+            "clocks": clk.summary(), "gpu_launches": K * (ser.nodes_launch_count(N) if nodes else ser.launch_count(M, N)),
+            "gpu_launches_note": ("per step: bbox, morton, pack_sources, pack_node_soa, block_boxes, sym_kernel, "
+                                  "nbr_kernel, finalize_nodes (+ CUB sort)" if nodes else
+                                  "per step: bbox, 2 morton, pack sources, pack targets, fused far+near, finalize "
+                                  "(+ CUB sort)"),
             "e2e": None}
     if not args.no_cpu_baseline:  # the oracle's sharp mode on a target sample, host cores
         import oracle
@@ -999,6 +1012,8 @@ def run_eval(args, rank, world):
                                        "(sharding.evaluate_sharded), sources replicated, all-gather of u, v in the "
                                        "timed region")},
             "fp64_tflops_alg": alg_flops * K / total_s / 1e12,
+            "fp64_tflops_alg_note": "whole step, SURVEY 8(d) per-pair convention: 57 flops per far pair + 180 per "
+                                    "near pair, every directed pair counted",
             "roofline": roofline, "clocks": clocks, "parity": parity,
             "gpu_launches": K * (ser.nodes_launch_count(N, 3) if nodes else
                                  ser.launch_count(M_loc, N, 3) + (0 if fused else 1)),

@@ -7,8 +7,9 @@
 // shared part serves both directions.
 //
 // Pipeline (after K0 sort/pack of the general path):
-//   pack_node_soa      node records as SoA 32-node tiles [Npad/32][13][32]
-//                      (x | m w | f w | q | alpha) and the node-target fields
+//   pack_node_soa      node records in 32-node tiles (x | m w | f w | q | alpha; 14-double
+//                      AoS records by default, SoA [13][32] with SER_SYM_AOS=0) and the
+//                      node-target fields
 //   block_boxes        64-node block boxes (union of the two 32-node boxes)
 //   sym_kernel         K5: every unordered pair of 64-node blocks (m < n) whose
 //                      boxes are beyond the cutoff ("AF": all far) -- both
@@ -20,9 +21,10 @@
 //                      K6 partials, applies 1/(8 pi), -6 and chi q0 = q/2 (b = 0; a shard other
 //                      than 0 of a sharded call adds no chi term: the shards' sum has it once)
 //
-// Determinism: sym_kernel assigns items to CTAs statically (item i -> CTA
-// i mod G) and every CTA accumulates into its OWN slice of the workspace, in
-// item order; finalize sums the slices in CTA order.  No atomics on data.
+// Determinism: sym_kernel assigns items to CTAs statically (CTA g takes the g-th
+// contiguous range of the c-major item list) and every CTA accumulates into its OWN
+// slice of the workspace, in item order; finalize sums the slices in CTA order.
+// No atomics on data.
 #pragma once
 #include "kernels.cuh"
 
