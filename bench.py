@@ -137,13 +137,18 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def pad(self, busy, min_samples=5, limit_s=5.0):
+    def pad(self, busy, min_samples=5, limit_s=5.0, agree=None):
         """Short timed regions see few 50 ms samples: keep the GPU busy with untimed steps
-        (`busy()`) until the record holds `min_samples` (clocks under the same load)."""
-        if self.proc is None:
-            return
+        (`busy()`) until the record holds `min_samples` (clocks under the same load).
+        `agree(flag) -> bool` (multi-rank runs) makes every rank take the same decision, so
+        ranks whose steps run collectives stay in step."""
         t0 = time.time()
-        while len(self.lines) < min_samples and time.time() - t0 < limit_s:
+        while True:
+            need = self.proc is not None and len(self.lines) < min_samples and time.time() - t0 < limit_s
+            if agree is not None:
+                need = agree(need)
+            if not need:
+                return
             busy()
 
     def _read(self):
@@ -847,7 +852,13 @@ def run_eval(args, rank, world):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize(dev)
-        clk.pad(lambda: (step(), torch.cuda.synchronize(dev)))
+        def agree(flag):  # any rank still short of samples -> every rank pads one more step
+            if dist is None:
+                return flag
+            t = torch.tensor([1.0 if flag else 0.0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return bool(t.item() > 0)
+        clk.pad(lambda: (step(), torch.cuda.synchronize(dev)), agree=agree)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     pair_ms = [a.elapsed_time(b) for a, b in evp]
     near_ms = [a.elapsed_time(b) for a, b in evn]
