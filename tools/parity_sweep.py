@@ -8,7 +8,7 @@ b ~ U[-4h, 4h], a few far targets), then compares stokes_er_eval with the oracle
 mode (max-norm relative, u and v separately; the bar is 1e-12).  Every fifth case also runs
 the on-surface s# variant (random delta in [2h, 4h], cutoff 7) on the node targets, and every
 fourth the treecode (random N0 in [40, 600), p in [2, 8], theta in [0.3, 0.8]) against the
-treecode oracle.
+treecode oracle, and every third the node-target path (stokes_er_eval_nodes) on all the nodes.
 
     python tools/parity_sweep.py OUT.json [n_cases]
 """
@@ -27,7 +27,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import oracle  # noqa: E402  (test infrastructure: this is a parity check)
 import paper_2507_00156_b200 as ser  # noqa: E402
-from workloads.configs import make_block, random_directions  # noqa: E402
+from workloads.configs import make_block, node_block, random_directions  # noqa: E402
 from workloads.densities import PolyField, TrigField  # noqa: E402
 from workloads.quadrature import Ellipsoid, ellipsoid_closest_point, quadrature  # noqa: E402
 
@@ -98,12 +98,21 @@ def main(out, n_cases=60):
                 row["tree_rel_u"] = rel(ut.cpu().numpy(), utr)
             if mode & 2:
                 row["tree_rel_v"] = rel(vt.cpu().numpy(), vtr)
+        if seed % 3 == 2:  # node targets: stokes_er_eval_nodes (symmetric far kernel) on every node
+            nb = node_block(blk)
+            un, vn = ser.evaluate_nodes_block(nb, mode=mode)
+            unr, vnr = oracle.evaluate_block(nb, mode=mode, localized=True)
+            if mode & 1:
+                row["nodes_rel_u"] = rel(un.cpu().numpy(), unr)
+            if mode & 2:
+                row["nodes_rel_v"] = rel(vn.cpu().numpy(), vnr)
         rows.append(row)
         print(row, flush=True)
-    worst = max(v for r in rows for k, v in r.items() if k.startswith(("rel_", "sharp_rel_", "tree_rel_")))
+    worst = max(v for r in rows for k, v in r.items() if k.startswith(("rel_", "sharp_rel_", "tree_rel_", "nodes_rel_")))
     res = {"what": "randomized parity sweep: stokes_er_eval (every 5th case also stokes_er_eval_onsurface, every "
-                   "4th also stokes_er_eval_tree with random N0, p, theta) vs the oracle's localized mode "
-                   "(treecode: vs the treecode oracle), max-norm relative per output",
+                   "4th also stokes_er_eval_tree with random N0, p, theta, every 3rd also stokes_er_eval_nodes on "
+                   "all nodes) vs the oracle's localized mode (treecode: vs the treecode oracle), max-norm "
+                   "relative per output",
            "cases": len(rows), "worst_rel": worst, "bar": 1e-12, "pass": bool(worst <= 1e-12),
            "seconds": time.time() - t0, "rows": rows}
     json.dump(res, open(out, "w"), indent=1)
