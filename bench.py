@@ -81,6 +81,9 @@ def parse():
     ap.add_argument("--path", choices=["auto", "general", "nodes"], default="auto",
                     help="nodes: stokes_er_eval_nodes (targets = the nodes, symmetric far kernel); general: "
                          "stokes_er_eval; auto: nodes when the workload's targets are its nodes (config 5) on 1 GPU")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="time CUDA-graph replays of the evaluation (captured once after the warm-up; the same "
+                         "kernels, without the per-call host enqueue on the timeline); auto: on for 1 GPU")
     ap.add_argument("--schedule", choices=["fused", "separate"], default="fused",
                     help="fused: one persistent kernel, far items and near items from one interleaved "
                          "queue (default); separate: far kernel then near kernel")
@@ -810,7 +813,7 @@ def run_eval(args, rank, world):
         opt.near_kernel_start_event = ev_near[0].cuda_event if ev_near else None
         opt.near_kernel_end_event = ev_near[1].cuda_event if ev_near else None
         return ser.evaluate(sx, sn, sw, f, q, ty, tb, tx, h, rho, mode=mode, out_u=ou, out_v=ov, workspace=ws,
-                            stream=stream, options=opt)
+                            stream=torch.cuda.current_stream(dev), options=opt)
 
     def step(ev_pair=None, ev_near=None):
         if nodes:
@@ -820,8 +823,8 @@ def run_eval(args, rank, world):
             opt.near_kernel_end_event = ev_near[1].cuda_event if ev_near else None
             if world > 1:  # shard r of the block-pair items + one all-reduce of u, v
                 return nodes_sharded_step(arrs[:5], block, opt, ws, stream)
-            ser.evaluate_nodes(*arrs[:5], block.h, block.rho, out_u=out_u, out_v=out_v, workspace=ws, stream=stream,
-                               options=opt)
+            ser.evaluate_nodes(*arrs[:5], block.h, block.rho, out_u=out_u, out_v=out_v, workspace=ws,
+                               stream=torch.cuda.current_stream(dev), options=opt)
             return out_u, out_v
         if world == 1:
             local_eval(*arrs, block.h, block.rho, ev_pair=ev_pair, ev_near=ev_near, ou=out_u, ov=out_v)
@@ -839,6 +842,19 @@ def run_eval(args, rank, world):
     for a, b in evp + evn:  # torch creates the CUDA event lazily on first record: materialize the handles
         a.record(stream)
         b.record(stream)
+    # 1 GPU: capture the evaluation once (the library only enqueues: no host sync, no allocation) and time
+    # replays, so a small step's kernels are not spaced out by the Python + ctypes enqueue of each call;
+    # the graph holds one pair of kernel events, read after each replay
+    graph = None
+    if world == 1 and args.graph != "off":
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(evp[0], evn[0])
+        torch.cuda.synchronize(dev)
+        graph.replay()  # a first replay outside the timed region
+        torch.cuda.synchronize(dev)
+    g_pair, g_near = [], []
     with ClockSampler(local) as clk:
         if dist is not None:
             dist.barrier()
@@ -846,8 +862,16 @@ def run_eval(args, rank, world):
         for i in range(K):
             flush.zero_()  # L2 flush, outside the timed events
             ev[i][0].record(stream)
-            res_u, res_v = step(evp[i], evn[i])
+            if graph is not None:
+                graph.replay()
+                res_u, res_v = out_u, out_v
+            else:
+                res_u, res_v = step(evp[i], evn[i])
             ev[i][1].record(stream)
+            if graph is not None:  # this replay's kernel events (the host sync is outside the timed events)
+                torch.cuda.synchronize(dev)
+                g_pair.append(evp[0][0].elapsed_time(evp[0][1]))
+                g_near.append(evn[0][0].elapsed_time(evn[0][1]) if (nodes or not fused) else 0.0)
         torch.cuda.synchronize(dev)
         if dist is not None:
             dist.barrier()
@@ -860,8 +884,8 @@ def run_eval(args, rank, world):
             return bool(t.item() > 0)
         clk.pad(lambda: (step(), torch.cuda.synchronize(dev)), agree=agree)
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    pair_ms = [a.elapsed_time(b) for a, b in evp]
-    near_ms = [a.elapsed_time(b) for a, b in evn]
+    pair_ms = g_pair if graph is not None else [a.elapsed_time(b) for a, b in evp]
+    near_ms = g_near if graph is not None else [a.elapsed_time(b) for a, b in evn]
     total_s = max_over_ranks(sum(step_ms) / 1e3, dev)
     value = pairs * K / total_s
     u_host, v_host = res_u.cpu().numpy(), res_v.cpu().numpy()
@@ -974,7 +998,8 @@ def run_eval(args, rank, world):
                 "flops_per_launch": k_flops, "flop_convention": conv,
                 "frac_issued_convention": k_issued / far_avg_s / 1e12 / peak,
                 "kernel_ms": far_avg_s * 1e3, "kernel_share": sum(pair_ms) / sum(step_ms),
-                "timing": "CUDA events recorded by the library around the kernel on the launching stream",
+                "timing": "CUDA events recorded by the library around the kernel on the launching stream"
+                          + (" (inside the captured graph, read after each replay)" if graph is not None else ""),
                 "far_pairs": far, "near_pairs": near}
     traffic = committed_traffic(bench_cfg, kprefix)
     if traffic:
@@ -1015,6 +1040,9 @@ def run_eval(args, rank, world):
                        "grid_ctas": int(opt.stats[1]), "chunk_tiles": int(opt.stats[2]),
                        "schedule": "nodes" if nodes else args.schedule,
                        "path": "stokes_er_eval_nodes" if nodes else "stokes_er_eval",
+                       "launch": ("CUDA-graph replay of one evaluation (captured once after the warm-up; the "
+                                  "library's kernels, timed by events on the replay stream)" if graph is not None
+                                  else "eager (one C-ABI call per step)"),
                        "parallelism": ("single GPU" if world == 1 else
                                        f"node-path shards x{world}: 1/{world} of the symmetric kernel's block-pair "
                                        "items and of the neighbour units per rank (sharding.evaluate_nodes_sharded), "
@@ -1031,9 +1059,12 @@ def run_eval(args, rank, world):
             "gpu_launches_note": ("our kernels per step: bbox, morton, pack_sources, pack_node_soa, block_boxes, "
                                   "sym_kernel, nbr_kernel, finalize_nodes (+ CUB radix-sort launches, library code)"
                                   if nodes else
-                                  "our kernels per step and rank: bbox, 2 morton, pack_sources, pack_targets, "
-                                  + ("fused far+near" if fused else "far, near") + ", finalize "
-                                  "(+ CUB radix-sort launches, library code)"),
+                                  ("our kernels per step and rank: small_rank, pack_both, "
+                                   if ser.launch_count(M_loc, N, 3) == 4 else
+                                   "our kernels per step and rank: bbox, 2 morton, pack_sources, pack_targets, ")
+                                  + ("fused far+near" if fused else "far, near") + ", finalize"
+                                  + ("" if ser.launch_count(M_loc, N, 3) == 4 else
+                                     " (+ CUB radix-sort launches, library code)")),
             "e2e": e2e}
     if near_info is not None:
         line["near_kernel"] = near_info

@@ -154,12 +154,14 @@ int stokes_er_eval_onsurface(const double* src_xyz, const double* src_normal, co
                              void* stream);
 
 /* Number of kernel launches one stokes_er_eval(M, N, mode) enqueues (ours; 4 when N, M <= 8192: the
- * one-CTA sort prologue; 7 otherwise, plus the CUB radix-sort launches). */
+ * counting-rank Morton prologue in one launch, no memset; 7 otherwise, plus the CUB radix-sort launches). */
 int stokes_er_launch_count(int64_t M, int64_t N, int mode);
 
 /* Optional profiling hooks for bench.py: if non-NULL, cudaEvent_t handles
  * (as void*) recorded on `stream` immediately before / after the far-field
- * pair-sum kernel (the dominant kernel) of this stokes_er_eval_ex call. */
+ * pair-sum kernel (the dominant kernel) of this stokes_er_eval_ex call.  While
+ * `stream` is being captured into a CUDA graph they are captured as external
+ * event-record nodes (cudaEventRecordExternal), so each replay records them. */
 typedef struct {
   void* pair_kernel_start_event;
   void* pair_kernel_end_event;
@@ -168,7 +170,7 @@ typedef struct {
   int64_t stats[4];       /* out: [0] work items, [1] grid CTAs, [2] chunk tiles, [3] targets/thread */
   void* near_kernel_start_event; /* optional events around the near-field kernel */
   void* near_kernel_end_event;
-  int near_phases;               /* 0 = automatic; near work units per 32-target group (1..64) */
+  int near_phases;               /* 0 = automatic; near work units per 32-target group (1..128; node path 1..64) */
   int schedule;                  /* STOKES_ER_SCHEDULE_FUSED (0, default): one persistent kernel whose
                                     CTAs take far items (a target block x a source chunk) and near
                                     items (one near unit per warp) from one queue that interleaves

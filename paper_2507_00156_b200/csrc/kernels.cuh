@@ -33,7 +33,6 @@
 
 #include <cuda_runtime.h>
 
-#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cstdint>
 #include <cstring>
@@ -184,15 +183,20 @@ __global__ void bbox_kernel(const double* __restrict__ sx, int64_t N, const doub
   }
 }
 
-// 30-bit Morton key of point i of x [3][n] in the box (blo, bhi).
+// 30-bit Morton key of point i of x [3][n] in the box with corner blo and per-axis scale
+// 1023 / extent (morton_scale): 10 bits per axis.
+__device__ __forceinline__ void morton_scale(const double (&blo)[3], const double (&bhi)[3], double (&sc)[3]) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) sc[d] = 1023.0 / fmax(bhi[d] - blo[d], 1e-300);
+}
 __device__ __forceinline__ uint32_t morton_key(const double* __restrict__ x, int64_t n, int64_t i,
-                                               const double (&blo)[3], const double (&bhi)[3]) {
+                                               const double (&blo)[3], const double (&sc)[3]) {
   uint32_t key = 0;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    const double ext = fmax(bhi[d] - blo[d], 1e-300);
-    double s = (x[d * n + i] - blo[d]) / ext * 1023.0;
-    s = fmin(fmax(s, 0.0), 1023.0);
+    double s = (x[d * n + i] - blo[d]) * sc[d];
+    s = s > 0.0 ? s : 0.0;  // plain selects: no NaN-propagation sequence per bound
+    s = s < 1023.0 ? s : 1023.0;
     key |= spread10(static_cast<uint32_t>(s)) << d;
   }
   return key;
@@ -204,75 +208,107 @@ __global__ void morton_kernel(const double* __restrict__ x, int64_t n, const lon
   if (i >= n) return;
   const double blo[3] = {dkey_inv(box[0]), dkey_inv(box[1]), dkey_inv(box[2])};
   const double bhi[3] = {dkey_inv(box[3]), dkey_inv(box[4]), dkey_inv(box[5])};
-  keys[i] = morton_key(x, n, i, blo, bhi);
+  double sc[3];
+  morton_scale(blo, bhi, sc);
+  keys[i] = morton_key(x, n, i, blo, sc);
   vals[i] = static_cast<int32_t>(i);
 }
 
-// Small problems (N, M <= kSmallSort): bounding box, Morton keys and a stable radix sort of the
-// sources (CTA 0) and of the targets (CTA 1) in ONE launch (the same keys and the same stable
-// order as bbox_kernel + morton_kernel + the CUB device sorts, so the same sums), instead of ~15.
-constexpr int kSmallSortThreads = 1024, kSmallSortItems = 8;
-constexpr int64_t kSmallSort = (int64_t)kSmallSortThreads * kSmallSortItems;
-constexpr int kSmallSortSmem =
-    (int)sizeof(typename cub::BlockRadixSort<uint32_t, kSmallSortThreads, kSmallSortItems, int32_t>::TempStorage);
-__global__ void __launch_bounds__(kSmallSortThreads, 1) small_sort_kernel(const double* __restrict__ sx, int64_t N,
-                                                                         const double* __restrict__ tx, int64_t M,
-                                                                         int32_t* __restrict__ svout,
-                                                                         int32_t* __restrict__ tvout) {
-  using Sort = cub::BlockRadixSort<uint32_t, kSmallSortThreads, kSmallSortItems, int32_t>;
-  extern __shared__ __align__(16) unsigned char small_smem[];  // kSmallSortSmem bytes (dynamic: > 48 KB)
-  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(small_smem);
-  __shared__ double red[kSmallSortThreads / 32][6];
+// Small problems (N, M <= kSmallSort): the Morton order by counting, in ONE launch of many CTAs
+// (instead of bbox + 2 morton + the CUB device sorts, ~15 launches). The position of point i in
+// the stable sort by key -- the order the large path's CUB sorts produce from the same keys -- is
+//   rank(i) = #{j < i : key_j <= key_i} + #{j > i : key_j < key_i}.
+// CTA c takes 32 points (lane = point) of the sources (c < ceil(N/32)) or of the targets; it
+// recomputes the common bounding box (exact min/max: the same frame as bbox_kernel) and every key
+// of that array into shared memory; its 16 warps count over 16 slices of j, four keys per 16-B
+// broadcast read: slices below the CTA's points use <=, slices above use <, and the few keys among
+// the CTA's own points take the exact (key, index) comparison. The slice counts are added in a
+// fixed order and perm[rank(i)] = i is written: integer counts, so the permutation is exact and
+// deterministic.
+constexpr int64_t kSmallSort = 8192;
+constexpr int kRankThreads = 512, kRankWarps = kRankThreads / 32, kRankPts = 32;
+__global__ void __launch_bounds__(kRankThreads) small_rank_kernel(const double* __restrict__ sx, int64_t N,
+                                                                 const double* __restrict__ tx, int64_t M,
+                                                                 int32_t* __restrict__ svout,
+                                                                 int32_t* __restrict__ tvout,
+                                                                 int* __restrict__ counters) {
+  __shared__ __align__(16) uint32_t skey[kSmallSort];
+  __shared__ double red[kRankWarps][6];
+  __shared__ double sbox[6];
+  __shared__ int cnt[kRankWarps][kRankPts];
+  if (blockIdx.x == 0 && threadIdx.x < 2) counters[threadIdx.x] = 0;  // the pair kernel's queues (no memset)
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int64_t i = threadIdx.x; i < N + M; i += kSmallSortThreads) {
+#pragma unroll 4
+  for (int64_t i = tid; i < N + M; i += kRankThreads) {  // independent loads in flight (latency-bound)
     const double* x = i < N ? sx + i : tx + (i - N);
     const int64_t n = i < N ? N : M;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      lo[d] = fmin(lo[d], x[d * n]);
-      hi[d] = fmax(hi[d], x[d * n]);
+    for (int d = 0; d < 3; ++d) {  // min/max: exact and order-free (plain selects)
+      const double v = x[d * n];
+      lo[d] = v < lo[d] ? v : lo[d];
+      hi[d] = v > hi[d] ? v : hi[d];
     }
   }
 #pragma unroll
   for (int d = 0; d < 3; ++d)
     for (int o = 16; o; o >>= 1) {
-      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
-      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+      const double a = __shfl_xor_sync(0xffffffffu, lo[d], o), b = __shfl_xor_sync(0xffffffffu, hi[d], o);
+      lo[d] = a < lo[d] ? a : lo[d];
+      hi[d] = b > hi[d] ? b : hi[d];
     }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0)
+  if (lane == 0)
     for (int d = 0; d < 3; ++d) { red[w][d] = lo[d]; red[w][3 + d] = hi[d]; }
   __syncthreads();
-  double blo[3], bhi[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {  // every thread reduces the 32 warp results (min/max: exact, order-free)
-    blo[d] = red[0][d];
-    bhi[d] = red[0][3 + d];
-    for (int k = 1; k < kSmallSortThreads / 32; ++k) {
-      blo[d] = fmin(blo[d], red[k][d]);
-      bhi[d] = fmax(bhi[d], red[k][3 + d]);
-    }
+  if (tid < 6) {  // one thread per box field reduces the warps' results
+    double v = red[0][tid];
+    for (int k = 1; k < kRankWarps; ++k)
+      v = tid < 3 ? (red[k][tid] < v ? red[k][tid] : v) : (red[k][tid] > v ? red[k][tid] : v);
+    sbox[tid] = v;
   }
-  {
-    const int pass = blockIdx.x;  // CTA 0 sorts the sources, CTA 1 the targets (both computed the same box)
-    const double* x = pass == 0 ? sx : tx;
-    const int64_t n = pass == 0 ? N : M;
-    int32_t* out = pass == 0 ? svout : tvout;
-    uint32_t keys[kSmallSortItems];
-    int32_t vals[kSmallSortItems];
+  __syncthreads();
+  const double blo[3] = {sbox[0], sbox[1], sbox[2]}, bhi[3] = {sbox[3], sbox[4], sbox[5]};
+  double sc[3];
+  morton_scale(blo, bhi, sc);
+  const int64_t cs = (N + kRankPts - 1) / kRankPts;
+  const bool is_src = blockIdx.x < cs;
+  const double* x = is_src ? sx : tx;
+  const int n = static_cast<int>(is_src ? N : M);
+  int32_t* out = is_src ? svout : tvout;
+  const int base = static_cast<int>((is_src ? blockIdx.x : blockIdx.x - cs) * kRankPts);
+  const int nq = (n + 3) >> 2;  // keys padded to whole quads with 0xffffffff (never counted)
+#pragma unroll 4
+  for (int j = tid; j < 4 * nq; j += kRankThreads) skey[j] = j < n ? morton_key(x, n, j, blo, sc) : 0xffffffffu;
+  __syncthreads();
+  const int i = base + lane;
+  const uint32_t ki = i < n ? skey[i] : 0u;
+  const uint4* k4 = reinterpret_cast<const uint4*>(skey);
+  const int q0 = w * nq / kRankWarps, q1 = (w + 1) * nq / kRankWarps;
+  const int qa = base >> 2, qb = (base + kRankPts) >> 2;  // quads [qa, qb) hold the CTA's own points
+  int c = 0;
+#pragma unroll 4
+  for (int q = q0; q < min(q1, qa); ++q) {  // every j < every i of the CTA: key_j <= key_i counts
+    const uint4 k = k4[q];
+    c += (k.x <= ki) + (k.y <= ki) + (k.z <= ki) + (k.w <= ki);
+  }
+  for (int q = max(q0, qa); q < min(q1, qb); ++q) {  // among the CTA's points: the exact comparison
+    const uint4 k = k4[q];
+    const uint32_t kk[4] = {k.x, k.y, k.z, k.w};
 #pragma unroll
-    for (int k = 0; k < kSmallSortItems; ++k) {  // blocked arrangement: thread t holds t*ITEMS + k
-      const int64_t i = (int64_t)threadIdx.x * kSmallSortItems + k;
-      keys[k] = i < n ? morton_key(x, n, i, blo, bhi) : 0x3fffffffu;  // padding sorts last (stable)
-      vals[k] = static_cast<int32_t>(i);
-    }
-    __syncthreads();  // red read by every thread before tmp (may alias nothing, but keep the order simple)
-    Sort(tmp).Sort(keys, vals, 0, 30);
+    for (int t = 0; t < 4; ++t) c += (kk[t] < ki || (kk[t] == ki && 4 * q + t < i)) ? 1 : 0;
+  }
+#pragma unroll 4
+  for (int q = max(q0, qb); q < q1; ++q) {  // every j > every i: key_j < key_i counts
+    const uint4 k = k4[q];
+    c += (k.x < ki) + (k.y < ki) + (k.z < ki) + (k.w < ki);
+  }
+  cnt[w][lane] = c;
+  __syncthreads();
+  if (w == 0 && i < n) {
+    int r = 0;
 #pragma unroll
-    for (int k = 0; k < kSmallSortItems; ++k) {
-      const int64_t r = (int64_t)threadIdx.x * kSmallSortItems + k;
-      if (r < n) out[r] = vals[k];
-    }
+    for (int k = 0; k < kRankWarps; ++k) r += cnt[k][lane];
+    out[r] = i;
   }
 }
 

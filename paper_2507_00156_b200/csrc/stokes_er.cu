@@ -139,6 +139,9 @@ size_t cub_sort_bytes(int64_t n) {
   return bytes;
 }
 
+#ifndef SER_MAX_PHASES
+#define SER_MAX_PHASES 64  // near phases per 32-target group at most (small M)
+#endif
 Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override, int phases_override = 0) {
   Plan p;
   p.mode = mode;
@@ -190,17 +193,18 @@ Plan make_plan(int64_t M, int64_t N, int mode, int T, int chunk_override, int ph
   p.off_partial = take((size_t)p.n_items * 6 * TB * sizeof(double));
   // near units (32-target group, phase): >= ~4 per resident warp (148 SMs x 12 warps)
   const int64_t groups = p.Mpad / 32;
-  // (up to 64 phases when there are few groups: small M)
-  p.near_phases = static_cast<int>(std::min<int64_t>(groups >= 512 ? 16 : 64,
-                                                     std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));
-  if (phases_override > 0) p.near_phases = std::min(phases_override, 64);
+  // (up to 64 phases when there are few groups: small M; up to 128 below 32 groups, e.g. config 1's
+  // 16: measured -8% per step there, +5-10% at 125-200 groups)
+  const int64_t cap = groups >= 512 ? 16 : (groups < 32 ? 2 * SER_MAX_PHASES : SER_MAX_PHASES);
+  p.near_phases = static_cast<int>(std::min<int64_t>(cap, std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));
+  if (phases_override > 0) p.near_phases = std::min(phases_override, 2 * SER_MAX_PHASES);
   p.off_near = take((size_t)p.near_phases * p.Mpad * 6 * sizeof(double));
   p.off_counter = take(sizeof(int) * 4);
   p.total = off;
   return p;
 }
 
-// N, M small enough for the one-CTA sort prologue (small_sort_kernel, kernels.cuh)
+// N, M small enough for the counting-rank prologue (small_rank_kernel, kernels.cuh)
 bool small_problem(int64_t M, int64_t N) { return N <= kSmallSort && M <= kSmallSort; }
 
 bool rho_ok(const double* rho) {
@@ -239,13 +243,58 @@ int opt_chunk(const stokes_er_options* o) { return o ? o->source_chunk_tiles : 0
 int opt_phases(const stokes_er_options* o) { return o ? o->near_phases : 0; }
 int opt_schedule(const stokes_er_options* o) { return o ? o->schedule : STOKES_ER_SCHEDULE_FUSED; }
 
+// The caller's timing events (stokes_er_options): a plain record on the stream, or, while the stream
+// is being captured into a CUDA graph, an external event-record node (a plain cudaEventRecord would
+// only become a capture dependency, not a timestamp of each replay).
+void record_event(void* ev, cudaStream_t s) {
+  if (!ev) return;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(static_cast<cudaEvent_t>(ev), s);
+}
+
+// Launch facts computed once per device (and per kernel): the SM count and a kernel's resident
+// CTAs per SM after raising its dynamic-SMEM limit. Host-side only; it keeps the driver queries
+// (~µs each) off the enqueue path of small evaluations, whose kernels take ~0.1 ms.
+constexpr int kMaxDevices = 64;
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+int device_sms() {
+  static int cache[kMaxDevices];
+  const int dev = current_device();
+  int sms = (dev >= 0 && dev < kMaxDevices) ? cache[dev] : 0;
+  if (sms == 0) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < kMaxDevices) cache[dev] = sms;
+  }
+  return sms;
+}
+template <auto Kernel>
+int resident_ctas(int threads, int dyn_smem) {
+  static int cache[kMaxDevices][3];  // occupancy, threads, dyn_smem + 1
+  const int dev = current_device();
+  const bool ok = dev >= 0 && dev < kMaxDevices;
+  if (ok && cache[dev][1] == threads && cache[dev][2] == dyn_smem + 1) return cache[dev][0];
+  if (dyn_smem > 0) cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, Kernel, threads, dyn_smem);
+  if (ok) {
+    cache[dev][0] = occ;
+    cache[dev][1] = threads;
+    cache[dev][2] = dyn_smem + 1;
+  }
+  return occ;
+}
+
 template <int MODE, int T>
 void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(far_kernel<MODE, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFarSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, far_kernel<MODE, T>, kThreads, kFarSmemBytes);
+  const int sms = device_sms();
+  const int occ = resident_ctas<far_kernel<MODE, T>>(kThreads, kFarSmemBytes);
   const int grid = std::max(1, std::min(pp.n_items, sms * std::max(occ, 1)));
   *grid_out = grid;
   far_kernel<MODE, T><<<grid, kThreads, kFarSmemBytes, s>>>(pp);
@@ -253,9 +302,7 @@ void launch_pairs(const PairParams& pp, cudaStream_t s, int* grid_out) {
 
 template <int MODE, int T, bool SHARP>
 int launch_fused(const PairParams& pp, const NearParams& np, int n_near_items, int sms, cudaStream_t s) {
-  int occ = 0;
-  cudaFuncSetAttribute(fused_kernel<MODE, T, SHARP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<MODE, T, SHARP>, kThreads, kFusedSmemBytes);
+  const int occ = resident_ctas<fused_kernel<MODE, T, SHARP>>(kThreads, kFusedSmemBytes);
   const int64_t work = (int64_t)pp.n_items + n_near_items;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)sms * std::max(occ, 1))));
   fused_kernel<MODE, T, SHARP><<<grid, kThreads, kFusedSmemBytes, s>>>(pp, np, n_near_items);
@@ -288,12 +335,10 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
 
   Delta3 r3{{rho[0], rho[1], rho[2]}};
   if (small_problem(M, N)) {
-    // small problems: box, keys and both sorts in one CTA, both packs in one launch (the same
-    // Morton order and records as below, 2 launches instead of ~15)
-    if (cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSortSmem) !=
-        cudaSuccess)
-      return STOKES_ER_ECUDA;
-    small_sort_kernel<<<2, kSmallSortThreads, kSmallSortSmem, s>>>(sx, N, ty, M, svout, tvout);
+    // small problems: box, keys and both Morton orders in one launch (ranks by counting), both packs
+    // in one launch (the same order and records as below, 2 launches instead of ~15)
+    small_rank_kernel<<<static_cast<int>(ceil_div(N, kRankPts) + ceil_div(M, kRankPts)), kRankThreads, 0, s>>>(
+        sx, N, ty, M, svout, tvout, counter);
     pack_both<MODE><<<static_cast<int>(P.Npad / kTile + ceil_div(P.Mpad, kTile)), kTile, 0, s>>>(
         sx, sn, sw, f, q, N, P.Npad, svout, src, srcbox, ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt, orig);
   } else {
@@ -316,7 +361,8 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
     pack_targets<MODE><<<ceil_div(P.Mpad, 256), 256, 0, s>>>(ty, tb, x0d, M, P.Mpad, tvout, h, r3, SHARP, tgt,
                                                               orig);
   }
-  if (cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess) return STOKES_ER_ECUDA;
+  if (!small_problem(M, N) && cudaMemsetAsync(counter, 0, 2 * sizeof(int), s) != cudaSuccess)
+    return STOKES_ER_ECUDA;
 
   PairParams pp;
   pp.src = src;
@@ -350,36 +396,30 @@ int run_eval(const double* sx, const double* sn, const double* sw, const double*
   np.rc2_box = pp.rc2_box;
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = pp.inv_delta[k];
 
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   int grid = 0;
   if (opt_schedule(opt) == STOKES_ER_SCHEDULE_FUSED) {
     // one persistent kernel: far items and near items (kNearWarps units each) interleaved
     const int n_near_items = static_cast<int>(ceil_div(np.n_units, kNearWarps));
-    if (opt && opt->pair_kernel_start_event)
-      cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
+    if (opt) record_event(opt->pair_kernel_start_event, s);
     if (P.T == 4) grid = launch_fused<MODE, 4, SHARP>(pp, np, n_near_items, sms, s);
     else if (P.T == 3) grid = launch_fused<MODE, 3, SHARP>(pp, np, n_near_items, sms, s);
     else if (P.T == 1) grid = launch_fused<MODE, 1, SHARP>(pp, np, n_near_items, sms, s);
     else grid = launch_fused<MODE, 2, SHARP>(pp, np, n_near_items, sms, s);
-    if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
+    if (opt) record_event(opt->pair_kernel_end_event, s);
   } else {
-    if (opt && opt->pair_kernel_start_event)
-      cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
+    if (opt) record_event(opt->pair_kernel_start_event, s);
     if (P.T == 4) launch_pairs<MODE, 4>(pp, s, &grid);
     else if (P.T == 3) launch_pairs<MODE, 3>(pp, s, &grid);
     else if (P.T == 1) launch_pairs<MODE, 1>(pp, s, &grid);
     else launch_pairs<MODE, 2>(pp, s, &grid);
-    if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
-    if (opt && opt->near_kernel_start_event)
-      cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_start_event), s);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, near_kernel<MODE, SHARP>, kNearWarps * 32, 0);
+    if (opt) record_event(opt->pair_kernel_end_event, s);
+    if (opt) record_event(opt->near_kernel_start_event, s);
+    const int occ = resident_ctas<near_kernel<MODE, SHARP>>(kNearWarps * 32, 0);
     const int ngrid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(occ, 1))));
     near_kernel<MODE, SHARP><<<ngrid, kNearWarps * 32, 0, s>>>(np);
-    if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
+    if (opt) record_event(opt->near_kernel_end_event, s);
   }
   if (opt) {
     opt->stats[0] = P.n_items;
@@ -489,9 +529,7 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   const double dmax = rho[2] * h;
   const double cutoff = SHARP ? STOKES_ER_CUTOFF_SURFACE : STOKES_ER_CUTOFF;
   const double rc2 = (cutoff * dmax) * (cutoff * dmax);
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   TreeFarParams tfp;
   tfp.nodes = nodes;
   tfp.G = G;
@@ -520,15 +558,13 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
   for (int k = 0; k < 3; ++k) np.inv_delta[k] = 1.0 / (rho[k] * h);
   {  // one persistent kernel: tree walks of the target groups + the near units
     const int n_near = SER_TREE_FUSED_NEAR ? np.n_units : 0;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tree_far_kernel<MODE, SHARP>, kTreeWarps * 32, 0);
+    const int occ = resident_ctas<tree_far_kernel<MODE, SHARP>>(kTreeWarps * 32, 0);
     const int64_t work = (int64_t)tfp.n_groups + n_near;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(work, kTreeWarps), (int64_t)sms * std::max(occ, 1))));
     tree_far_kernel<MODE, SHARP><<<grid, kTreeWarps * 32, 0, s>>>(tfp, np, n_near);
     if (!SER_TREE_FUSED_NEAR) {
-      int nocc = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nocc, near_kernel<MODE, SHARP>, kNearWarps * 32, 0);
+      const int nocc = resident_ctas<near_kernel<MODE, SHARP>>(kNearWarps * 32, 0);
       const int ngrid = static_cast<int>(std::max<int64_t>(
           1, std::min<int64_t>(ceil_div(np.n_units, kNearWarps), (int64_t)sms * std::max(nocc, 1))));
       near_kernel<MODE, SHARP><<<ngrid, kNearWarps * 32, 0, s>>>(np);
@@ -691,20 +727,18 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
   if (cudaFuncSetAttribute(sym_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.sym_smem) !=
       cudaSuccess)
     return STOKES_ER_ECUDA;
-  if (opt && opt->pair_kernel_start_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_start_event), s);
+  if (opt) record_event(opt->pair_kernel_start_event, s);
   sym_kernel<MODE><<<P.G, kSymThreads, P.sym_smem, s>>>(sp);
-  if (opt && opt->pair_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->pair_kernel_end_event), s);
-  if (opt && opt->near_kernel_start_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_start_event), s);
+  if (opt) record_event(opt->pair_kernel_end_event, s);
+  if (opt) record_event(opt->near_kernel_start_event, s);
   {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, nbr_kernel<MODE, SHARP>, 64, 0);
+    const int sms = device_sms();
+    const int occ = resident_ctas<nbr_kernel<MODE, SHARP>>(64, 0);
     const int ngrid = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(np.n_units, 2), (int64_t)sms * std::max(occ, 1))));
     nbr_kernel<MODE, SHARP><<<ngrid, 64, 0, s>>>(np, blkbox, unit_base);
   }
-  if (opt && opt->near_kernel_end_event) cudaEventRecord(static_cast<cudaEvent_t>(opt->near_kernel_end_event), s);
+  if (opt) record_event(opt->near_kernel_end_event, s);
   if (opt) {
     opt->stats[0] = P.n_items;
     opt->stats[1] = P.G;
@@ -1031,7 +1065,7 @@ int stokes_er_launch_count(int64_t M, int64_t N, int mode) {
   // bbox, 2x morton, pack sources, pack targets, fused far+near, finalize: our
   // kernels (default schedule; STOKES_ER_SCHEDULE_SEPARATE adds one).  The two
   // CUB radix sorts add their own launches (library code).  Small problems (N, M <=
-  // 8192): small_sort, pack_both, fused far+near, finalize (no CUB launches).
+  // 8192): small_rank, pack_both, fused far+near, finalize (no CUB launches).
   if (M <= 0) return 0;
   return small_problem(M, N) ? 4 : 7;
 }

@@ -453,9 +453,10 @@ def test_wide_rho_ratio(ser, rho):
 
 @pytest.mark.parametrize("n", [8192, 8193])
 def test_small_sort_prologue_boundary(ser, n):
-    """N, M <= 8192 take the one-launch sort prologue (small_sort_kernel + pack_both), larger
-    problems bbox + morton + the CUB device sorts: both sides of the boundary against the oracle
-    (the first n nodes of the 1/h = 32 sphere as sources, a target sample of config 2)."""
+    """N, M <= 8192 take the one-launch Morton prologue (small_rank_kernel: ranks by counting,
+    + pack_both), larger problems bbox + morton + the CUB device sorts: both sides of the boundary
+    against the oracle (the first n nodes of the 1/h = 32 sphere as sources, a target sample of
+    config 2)."""
     import dataclasses
 
     blk = config2(inv_h=32)
