@@ -47,10 +47,28 @@ __device__ __forceinline__ double warp_sum(double v) {
 // coordinates (xi, eta) = ((x_k - x0).t1, (x_k - x0).t2) / R, i.e.
 // L = Q z with Phi = Q R (modified Gram-Schmidt over the warp) and R^T z = e_1
 // (the constant monomial is column 0).
-__global__ void stencil_kernel(const double* __restrict__ sx, int64_t Ns, const double* __restrict__ ty,
-                               const double* __restrict__ tb, const double* __restrict__ x0d, int64_t Nt,
-                               double R, int* __restrict__ cnt, int* __restrict__ idx, double* __restrict__ L,
-                               int* __restrict__ status) {
+// Bounding box [lo | hi] of each run of 32 consecutive source nodes (index order), for the
+// stencil scan's chunk culling.
+__global__ void chunk_box_kernel(const double* __restrict__ sx, int64_t Ns, double* __restrict__ box) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c * 32 >= Ns) return;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  const int64_t kend = (c * 32 + 32 < Ns) ? c * 32 + 32 : Ns;
+  for (int64_t k = c * 32; k < kend; ++k)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = fmin(lo[d], sx[d * Ns + k]);
+      hi[d] = fmax(hi[d], sx[d * Ns + k]);
+    }
+  for (int d = 0; d < 3; ++d) {
+    box[c * 6 + d] = lo[d];
+    box[c * 6 + 3 + d] = hi[d];
+  }
+}
+
+__global__ void stencil_kernel(const double* __restrict__ sx, int64_t Ns, const double* __restrict__ sbox,
+                               const double* __restrict__ ty, const double* __restrict__ tb,
+                               const double* __restrict__ x0d, int64_t Nt, double R, int* __restrict__ cnt,
+                               int* __restrict__ idx, double* __restrict__ L, int* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (t >= Nt) return;
@@ -58,19 +76,38 @@ __global__ void stencil_kernel(const double* __restrict__ sx, int64_t Ns, const 
   for (int d = 0; d < 3; ++d) n0[d] = x0d[d * Nt + t];
   const double b = tb[t];
   for (int d = 0; d < 3; ++d) x0[d] = ty[d * Nt + t] - b * n0[d];
-  const double R2 = R * R;
+  const double R2 = R * R, R2box = R2 * (1.0 + 1e-9);
   int count = 0;
-  for (int64_t base = 0; base < Ns; base += 32) {
-    const int64_t k = base + lane;
-    bool in = false;
-    if (k < Ns) {
-      const double dx = sx[k] - x0[0], dy = sx[Ns + k] - x0[1], dz = sx[2 * Ns + k] - x0[2];
-      in = dx * dx + dy * dy + dz * dz <= R2;
+  // chunks of 32 consecutive nodes whose box is within R of x0 (lane = chunk, ballot), then the
+  // nodes of each such chunk (lane = node): the same selection, in the same index order, as a scan
+  // over every node (round 1), at ~1/30 of the distance tests
+  const int64_t nch = (Ns + 31) / 32;
+  for (int64_t cb = 0; cb < nch; cb += 32) {
+    bool cand = false;
+    if (cb + lane < nch) {
+      const double* bx = sbox + (cb + lane) * 6;
+      double g2 = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        const double gap = fmax(0.0, fmax(bx[d] - x0[d], x0[d] - bx[3 + d]));
+        g2 = fma(gap, gap, g2);
+      }
+      cand = g2 <= R2box;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, in);
-    const int pos = count + __popc(m & ((1u << lane) - 1u));
-    if (in && pos < kKmax) idx[(int64_t)pos * Nt + t] = static_cast<int>(k);
-    count += __popc(m);
+    unsigned cm = __ballot_sync(0xffffffffu, cand);
+    while (cm) {
+      const int64_t base = (cb + __ffs(cm) - 1) * 32;
+      cm &= cm - 1;
+      const int64_t k = base + lane;
+      bool in = false;
+      if (k < Ns) {
+        const double dx = sx[k] - x0[0], dy = sx[Ns + k] - x0[1], dz = sx[2 * Ns + k] - x0[2];
+        in = dx * dx + dy * dy + dz * dz <= R2;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      const int pos = count + __popc(m & ((1u << lane) - 1u));
+      if (in && pos < kKmax) idx[(int64_t)pos * Nt + t] = static_cast<int>(k);
+      count += __popc(m);
+    }
   }
   if (count < kNpoly || count > kKmax) {
     if (lane == 0) {
@@ -433,7 +470,9 @@ int stokes_er_twodrop_setup(const stokes_er_drop drops[2], const stokes_er_cross
     if (!st) st = ok(cudaMemsetAsync(x0c + 6 * Nb, 0, 3 * row, c.s));
     if (!st) st = ok(cudaMemsetAsync(c.at<double>(c.L.off_zero[b]), 0, row, c.s));
     if (st) break;
-    stencil_kernel<<<cdiv(Nb * 32, 128), 128, 0, c.s>>>(drops[m].xyz, drops[m].N, drops[b].xyz, cross[b].b,
+    double* sbox = c.at<double>(c.L.off_eval);  // the block evaluations' workspace is free during setup
+    chunk_box_kernel<<<cdiv(cdiv(drops[m].N, 32), 128), 128, 0, c.s>>>(drops[m].xyz, drops[m].N, sbox);
+    stencil_kernel<<<cdiv(Nb * 32, 128), 128, 0, c.s>>>(drops[m].xyz, drops[m].N, sbox, drops[b].xyz, cross[b].b,
                                                         cross[b].x0d, Nb, kInterpRadius * params->h,
                                                         c.at<int>(c.L.off_cnt[b]), c.at<int>(c.L.off_idx[b]),
                                                         c.at<double>(c.L.off_L[b]), status);
