@@ -202,6 +202,33 @@ def test_source_permutation_invariance(ser):
     assert rel(b[0], a[0]) <= 1e-13 and rel(b[1], a[1]) <= 1e-13
 
 
+def test_small_path_permutation_invariance(ser):
+    """N, M <= 8192 (the counting-rank Morton prologue): the sums do not depend on the input order of
+    the sources or of the targets (each order gives the same stable Morton order up to equal keys, so
+    equal results to rounding), including a duplicated node (equal keys: ties broken by index)."""
+    import dataclasses
+
+    blk = config1()
+    k = 5
+    cat = lambda a, b: np.ascontiguousarray(np.concatenate([a, b], axis=-1))
+    blk = dataclasses.replace(blk, src_xyz=cat(blk.src_xyz, blk.src_xyz[:, :k]),
+                              src_normal=cat(blk.src_normal, blk.src_normal[:, :k]),
+                              src_weight=cat(blk.src_weight, 0.25 * blk.src_weight[:k]),
+                              f=cat(blk.f, blk.f[:, :k]), q=cat(blk.q, blk.q[:, :k]))
+    rng = np.random.default_rng(5)
+    ps, pt = rng.permutation(blk.N), rng.permutation(blk.M)
+    pb = dataclasses.replace(blk, src_xyz=np.ascontiguousarray(blk.src_xyz[:, ps]),
+                             src_normal=np.ascontiguousarray(blk.src_normal[:, ps]),
+                             src_weight=np.ascontiguousarray(blk.src_weight[ps]),
+                             f=np.ascontiguousarray(blk.f[:, ps]), q=np.ascontiguousarray(blk.q[:, ps]))
+    pb = pb.take_targets(pt)
+    assert ser.launch_count(blk.M, blk.N) == 4
+    a = run_gpu(ser, blk)
+    b = run_gpu(ser, pb)
+    assert rel(b[0], a[0][:, pt]) <= 1e-13 and rel(b[1], a[1][:, pt]) <= 1e-13
+    check_block(ser, pb, localized=False)
+
+
 def test_host_entry_point_matches_device(ser):
     blk = config1()
     ud, vd = run_gpu(ser, blk)
