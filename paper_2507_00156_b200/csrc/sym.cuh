@@ -51,12 +51,6 @@ constexpr int kSymStages = 3;                              // R-block TMA ring
 #ifndef SER_SYM_PIPE
 #define SER_SYM_PIPE 0                                     // software-pipelined step (measured slower)
 #endif
-#ifndef SER_SYM_PREF
-#define SER_SYM_PREF 0                                     // next R position read one step ahead: tuning macro
-#endif
-#ifndef SER_SYM_DEPHASE
-#define SER_SYM_DEPHASE 0                                  // warps 4-7 pipelined, the others not: tuning macro
-#endif
 #ifndef SER_SYM_TR2
 #define SER_SYM_TR2 0                                      // 2 R nodes per step (4 pairs): tuning macro
 #endif
@@ -362,8 +356,8 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       const bool active = has_i && n > myblk && blocks_far(p.blk_box, myblk, n, p.rc2_box);
       const double* R = ring + st * 2 * kTileDoubles;
       if (active) {
-#if SER_SYM_PIPE || SER_SYM_DEPHASE
-       if (SER_SYM_PIPE || (SER_SYM_DEPHASE == 1 ? (warp >> 2) == 1 : (warp >> 2) >= 1)) {
+#if SER_SYM_PIPE
+       {
         // 64 steps over the R block's two 32-node halves; step kk pairs this lane's I nodes
         // with R node (lane + kk) & 31 of half kk >> 5 (lane-varying, conflict-free SoA reads);
         // the geometry of step kk + 1 is issued before the contractions of step kk (the last
@@ -398,9 +392,8 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
           g0 = n0;
           g1 = n1;
         }
-       } else
-#endif
-#if SER_SYM_TR2
+       }
+#elif SER_SYM_TR2
        {
         // both halves at once: step kk pairs the lane's two I nodes with R node (lane + kk) & 31 of
         // EACH half (4 independent pairs per step, two rotating accumulators)
@@ -423,32 +416,6 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
         rw += 32;
         rw[0 * kBlk] = rb.u0; rw[1 * kBlk] = rb.u1; rw[2 * kBlk] = rb.u2;
         rw[3 * kBlk] = rb.v0; rw[4 * kBlk] = rb.v1; rw[5 * kBlk] = rb.v2;
-       }
-#elif SER_SYM_PREF
-       {
-        // the next R node's position is read one step ahead (only x, y, z: 6 registers), so the
-        // head of a step (d, r^2, the MUFU seed) does not wait on shared memory
-#pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
-          Acc ra{0, 0, 0, 0, 0, 0};
-          const double* Rt = R + hf * kTileDoubles;
-          double2 pxy = *reinterpret_cast<const double2*>(Rt + nfield(lane, 0));
-          double pz = Rt[nfield(lane, 2)];
-#pragma unroll kSymUnroll
-          for (int kk = 0; kk < 32; ++kk) {
-            SymNode rn = load_node<MODE>(Rt, (lane + kk) & 31);
-            rn.x = pxy.x; rn.y = pxy.y; rn.z = pz;
-            const int nx = (lane + kk + 1) & 31;
-            pxy = *reinterpret_cast<const double2*>(Rt + nfield(nx, 0));
-            pz = Rt[nfield(nx, 2)];
-            sym_pair<MODE>(I0, rn, a0, ra);
-            sym_pair<MODE>(I1, rn, a1, ra);
-            shfl_acc(ra, (lane + 1) & 31);
-          }
-          double* rw = red + warp * 6 * kBlk + hf * 32 + lane;
-          rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
-          rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
-        }
        }
 #else
        {
