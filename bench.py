@@ -970,7 +970,7 @@ def run_eval(args, rank, world):
     if nodes:
         k_flops = sym_pairs / 2 * F_SYM_UNORDERED_ALG * share
         k_issued = sym_pairs / 2 * F_SYM_UNORDERED_ISSUED * share
-        kname = ("sym_kernel<3> (FP64 pipe): the far-field sum (PAPER.md:183-191) over all-far 64-node block "
+        kname = ("sym_kernel<3> (FP64 pipe): the far-field sum (PAPER.md:183-191) over all-far 96-node block "
                  "pairs, one evaluation of each pair's shared part for both directed pairs (node targets)")
         kprefix = "void ser::sym_kernel<3>"
         conv = (f"{F_SYM_UNORDERED_ALG} algorithmic flops per unordered far pair = {F_SYM_UNORDERED_ALG / 2} per "

@@ -577,7 +577,7 @@ int run_eval_tree(const double* sx, const double* sn, const double* sw, const do
 
 
 // ------------------------------------------------------------- node targets
-// stokes_er_eval_nodes (sym.cuh): the symmetric far kernel over 64-node block
+// stokes_er_eval_nodes (sym.cuh): the symmetric far kernel over kBlk-node (96-node) block
 // pairs + the neighbour units + finalize.  The plan depends on N only.
 struct NodePlan {
   int mode = 3;
@@ -603,7 +603,8 @@ NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
   NodePlan p;
   p.mode = mode;
   p.N = N;
-  p.Npad = ceil_div(N, kTile) * kTile;  // a multiple of 128: whole 64-node blocks and 128-target blocks
+  constexpr int64_t kPadUnit = kBlk % kTile == 0 ? kBlk : (kTile % kBlk == 0 ? kTile : (int64_t)kTile * kBlk / 32);
+  p.Npad = ceil_div(N, kPadUnit) * kPadUnit;  // whole symmetric blocks and 128-target blocks (384 = lcm(96, 128) for 96-node blocks)
   p.nb = static_cast<int>(p.Npad / kBlk);
   p.nsb = static_cast<int>(ceil_div(p.nb, kSymWarps));
   // R blocks per item: the largest multiple of the warp count (<= 4 of them, SMEM) that still

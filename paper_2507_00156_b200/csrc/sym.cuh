@@ -10,10 +10,10 @@
 //   pack_node_soa      node records in 32-node tiles (x | m w | f w | q | alpha; 14-double
 //                      AoS records by default, SoA [13][32] with SER_SYM_AOS=0) and the
 //                      node-target fields
-//   block_boxes        64-node block boxes (union of the two 32-node boxes)
-//   sym_kernel         K5: every unordered pair of 64-node blocks (m < n) whose
+//   block_boxes        kBlk-node block boxes (union of the kSymT = 3 32-node boxes)
+//   sym_kernel         K5: every unordered pair of kBlk-node (96-node) blocks (m < n) whose
 //                      boxes are beyond the cutoff ("AF": all far) -- both
-//                      directions of all 4096 pairs, far-field sums only
+//                      directions of all 9216 pairs, far-field sums only
 //   nbr_kernel         K6: per 32-target group, every source sub-tile of its own
 //                      block or of a block that is not AF: far pairs (masked)
 //                      and the near 3-delta pairs (the near unit's queue)
@@ -40,10 +40,15 @@ enum NodeField { NX = 0, NY, NZ, NMX, NMY, NMZ, NFX, NFY, NFZ, NQX, NQY, NQZ, NA
 constexpr int kNodeStride = SER_SYM_AOS ? 14 : kNodeFields;       // doubles per node in a tile
 constexpr int kTileDoubles = 32 * kNodeStride;                     // one 32-node tile
 __host__ __device__ constexpr int nfield(int l, int f) { return SER_SYM_AOS ? l * 14 + f : f * 32 + l; }
-constexpr int kBlk = 64;                                   // nodes per symmetric block (2 sub-tiles)
-constexpr int kBlkTileBytes = 2 * kTileDoubles * 8;        // one R block in SMEM (TMA unit)
+#ifndef SER_SYM_T
+#define SER_SYM_T 3                                        // I nodes per lane = 32-node sub-tiles per block
+                                                           // (3 at 8 warps: +2.9% over 2 at 12 warps; 4: -3%)
+#endif
+constexpr int kSymT = SER_SYM_T;
+constexpr int kBlk = 32 * kSymT;                           // nodes per symmetric block (96: 3 sub-tiles)
+constexpr int kBlkTileBytes = kSymT * kTileDoubles * 8;    // one R block in SMEM (TMA unit)
 #ifndef SER_SYM_WARPS
-#define SER_SYM_WARPS 12
+#define SER_SYM_WARPS 8
 #endif
 constexpr int kSymWarps = SER_SYM_WARPS;                   // I blocks per CTA (one per warp)
 constexpr int kSymThreads = kSymWarps * 32;
@@ -62,7 +67,7 @@ constexpr int kSymUnroll = SER_SYM_UNROLL;
 #define SER_SYM_MINB 1                                     // resident CTAs per SM (tuning macro)
 #endif
 #ifndef SER_SYM_MAXK
-#define SER_SYM_MAXK 4                                     // R blocks per item <= MAXK * warps (SMEM)
+#define SER_SYM_MAXK 3                                     // R blocks per item <= MAXK * warps (SMEM)
 #endif
 
 struct SymParams {
@@ -70,7 +75,7 @@ struct SymParams {
   const double* blk_box;  // [nb][8] lo xyz, pad, hi xyz, pad
   double* pacc;           // [G][6][Npad] per-CTA accumulators (zeroed by the host)
   int64_t Npad;
-  int nb;                 // 64-node blocks
+  int nb;                 // kBlk-node blocks
   int nsb;                // superblocks of kSymWarps blocks
   int chunk;              // R blocks per item (a multiple of kSymWarps)
   int nchunks;
@@ -79,7 +84,7 @@ struct SymParams {
   double rc2_box;
 };
 
-// Box-level "all far" test between 64-node blocks, symmetric in (a, b): every
+// Box-level "all far" test between kBlk-node blocks, symmetric in (a, b): every
 // pair has r^2 >= gap^2 > rc2 (1 + 1e-9).  The same expression decides which
 // pairs sym_kernel owns and which nbr_kernel owns.
 __device__ __forceinline__ bool blocks_far(const double* __restrict__ bb, int a, int b, double rc2_box) {
@@ -152,13 +157,17 @@ __global__ void pack_node_soa(const double* __restrict__ xyz, const double* __re
 __global__ void block_boxes(const double* __restrict__ box32, int nb, double* __restrict__ bb) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= nb) return;
-  const double* a = box32 + (int64_t)(2 * m) * 8;
-  const double* b = a + 8;
+  const double* a = box32 + (int64_t)(kSymT * m) * 8;
   double* o = bb + (int64_t)m * 8;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    o[d] = fmin(a[d], b[d]);
-    o[4 + d] = fmax(a[4 + d], b[4 + d]);
+    double lo = a[d], hi = a[4 + d];
+    for (int t = 1; t < kSymT; ++t) {
+      lo = fmin(lo, a[t * 8 + d]);
+      hi = fmax(hi, a[t * 8 + 4 + d]);
+    }
+    o[d] = lo;
+    o[4 + d] = hi;
   }
   o[3] = 0.0;
   o[7] = 0.0;
@@ -281,7 +290,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const SymParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
-  double* red = ring + kSymStages * 2 * kTileDoubles;
+  double* red = ring + kSymStages * kSymT * kTileDoubles;
   double* cacc = red + kSymWarps * 6 * kBlk;
   __shared__ __align__(8) uint64_t bar[kSymStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -331,20 +340,30 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
     const int first = n_first - r0;  // index of the first R block processed
     const bool has_i = myblk < p.nb;
 
-    // I block of this warp in registers (T = 2 nodes per lane)
+    // I block of this warp in registers (kSymT nodes per lane)
+#if SER_SYM_T == 2
     SymNode I0, I1;
     Acc a0{0, 0, 0, 0, 0, 0}, a1{0, 0, 0, 0, 0, 0};
     if (has_i) {
-      const double* t = p.nsoa + (int64_t)(2 * myblk) * kTileDoubles;
+      const double* t = p.nsoa + (int64_t)(kSymT * myblk) * kTileDoubles;
       I0 = load_node<MODE>(t, lane);
       I1 = load_node<MODE>(t + kTileDoubles, lane);
     }
+#else
+    SymNode I[kSymT];
+    Acc a[kSymT];
+#pragma unroll
+    for (int t = 0; t < kSymT; ++t) {
+      a[t] = Acc{0, 0, 0, 0, 0, 0};
+      if (has_i) I[t] = load_node<MODE>(p.nsoa + (int64_t)(kSymT * myblk + t) * kTileDoubles, lane);
+    }
+#endif
     __syncthreads();  // cacc ready; the previous item's readers of the ring are done
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       for (int b = 0; b < kSymStages && first + b < nr; ++b) {
         mbar_expect_tx(&bar[b], kBlkTileBytes);
-        bulk_g2s(ring + b * 2 * kTileDoubles, p.nsoa + (int64_t)(2 * (r0 + first + b)) * kTileDoubles,
+        bulk_g2s(ring + b * kSymT * kTileDoubles, p.nsoa + (int64_t)(kSymT * (r0 + first + b)) * kTileDoubles,
                  kBlkTileBytes, &bar[b]);
       }
     }
@@ -354,9 +373,28 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       phase_bits ^= 1u << st;
       const int n = r0 + ri;
       const bool active = has_i && n > myblk && blocks_far(p.blk_box, myblk, n, p.rc2_box);
-      const double* R = ring + st * 2 * kTileDoubles;
+      const double* R = ring + st * kSymT * kTileDoubles;
       if (active) {
-#if SER_SYM_PIPE
+#if SER_SYM_T != 2
+       {
+        // kSymT I nodes per lane share each R node read and each accumulator rotation
+#pragma unroll 1
+        for (int hf = 0; hf < kSymT; ++hf) {
+          Acc ra{0, 0, 0, 0, 0, 0};
+          const double* Rt = R + hf * kTileDoubles;
+#pragma unroll kSymUnroll
+          for (int kk = 0; kk < 32; ++kk) {
+            const SymNode rn = load_node<MODE>(Rt, (lane + kk) & 31);
+#pragma unroll
+            for (int t = 0; t < kSymT; ++t) sym_pair<MODE>(I[t], rn, a[t], ra);
+            shfl_acc(ra, (lane + 1) & 31);
+          }
+          double* rw = red + warp * 6 * kBlk + hf * 32 + lane;
+          rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
+          rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
+        }
+       }
+#elif SER_SYM_PIPE
        {
         // 64 steps over the R block's two 32-node halves; step kk pairs this lane's I nodes
         // with R node (lane + kk) & 31 of half kk >> 5 (lane-varying, conflict-free SoA reads);
@@ -440,13 +478,15 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
       } else {  // inactive warp: its share of this R block is zero
         double* rw = red + warp * 6 * kBlk + lane;
 #pragma unroll
-        for (int c = 0; c < 6; ++c) { rw[c * kBlk] = 0.0; rw[c * kBlk + 32] = 0.0; }
+        for (int c = 0; c < 6; ++c)
+#pragma unroll
+          for (int t = 0; t < kSymT; ++t) rw[c * kBlk + 32 * t] = 0.0;
       }
       __syncthreads();  // red complete; every warp is done reading ring[st]
       if (tid == 0 && ri + kSymStages < nr) {  // refill the stage just released
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[st], kBlkTileBytes);
-        bulk_g2s(ring + st * 2 * kTileDoubles, p.nsoa + (int64_t)(2 * (n + kSymStages)) * kTileDoubles,
+        bulk_g2s(ring + st * kSymT * kTileDoubles, p.nsoa + (int64_t)(kSymT * (n + kSymStages)) * kTileDoubles,
                  kBlkTileBytes, &bar[st]);
       }
       for (int x = tid; x < 6 * kBlk; x += kSymThreads) {  // fixed warp order: deterministic
@@ -460,12 +500,21 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
     }
     // flush: the I sums of every warp into this CTA's slice (the chunk's R sums when the chunk changes)
     if (has_i) {
+#if SER_SYM_T == 2
       const int64_t i0 = (int64_t)myblk * kBlk + lane, i1 = i0 + 32;
       double* a = my_acc;
       a[0 * p.Npad + i0] += a0.u0; a[1 * p.Npad + i0] += a0.u1; a[2 * p.Npad + i0] += a0.u2;
       a[3 * p.Npad + i0] += a0.v0; a[4 * p.Npad + i0] += a0.v1; a[5 * p.Npad + i0] += a0.v2;
       a[0 * p.Npad + i1] += a1.u0; a[1 * p.Npad + i1] += a1.u1; a[2 * p.Npad + i1] += a1.u2;
       a[3 * p.Npad + i1] += a1.v0; a[4 * p.Npad + i1] += a1.v1; a[5 * p.Npad + i1] += a1.v2;
+#else
+#pragma unroll
+      for (int t = 0; t < kSymT; ++t) {
+        const int64_t i = (int64_t)myblk * kBlk + 32 * t + lane;
+        my_acc[0 * p.Npad + i] += a[t].u0; my_acc[1 * p.Npad + i] += a[t].u1; my_acc[2 * p.Npad + i] += a[t].u2;
+        my_acc[3 * p.Npad + i] += a[t].v0; my_acc[4 * p.Npad + i] += a[t].v1; my_acc[5 * p.Npad + i] += a[t].v2;
+      }
+#endif
     }
     __syncthreads();  // I flush before any R flush (a diagonal chunk holds the same nodes)
   }
@@ -474,7 +523,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
 
 // ---------------------------------------------------------------- K6
 // Neighbour unit: 32 Morton-consecutive node targets (lane = target) x every
-// source sub-tile of their own 64-node block or of a block that is not AF with
+// source sub-tile of their own kBlk-node block or of a block that is not AF with
 // it (blocks_far false): exactly the directed pairs sym_kernel does not own.
 // Far pairs of those sub-tiles (r^2 > rc2) are summed here with the near pairs
 // masked (far_pair_masked); near pairs go through the near unit's per-lane queue
@@ -495,7 +544,7 @@ __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __re
   const int n_sub = static_cast<int>(p.Npad / kSub);
   const int64_t g = unit / p.phases;
   const int phase = unit - static_cast<int>(g) * p.phases;
-  const int tblk = static_cast<int>(g >> 1);
+  const int tblk = static_cast<int>(g / kSymT);
   const int64_t ti = g * 32 + lane;
   Tgt tg;
   tg.y0 = p.tgt[F_Y0 * p.Mpad + ti];
@@ -527,7 +576,7 @@ __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __re
   for (;;) {
     while (mm == 0 && base < n_sub) {
       const int sb = base + lane;
-      const bool sel = sb < n_sub && ((sb >> 1) == tblk || !blocks_far(blk_box, tblk, sb >> 1, p.rc2_box));
+      const bool sel = sb < n_sub && (sb / kSymT == tblk || !blocks_far(blk_box, tblk, sb / kSymT, p.rc2_box));
       mm = __ballot_sync(0xffffffffu, sel);
       unsigned keep = 0, m = mm;
       while (m) {

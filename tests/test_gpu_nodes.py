@@ -5,7 +5,7 @@ nodes, b = 0, x0d = [n; f; q] (workloads.configs.node_block).  Tolerance as in
 test_gpu_parity.py (north_star): max-norm relative <= 1e-12 per field.  The symmetric far
 kernel shares each far pair's geometry between (i <- j) and (j <- i); the neighbour units own
 every pair of a block pair that is not all-far.  These tests cover both owners, their
-boundary (64-node block boxes), padding, ragged N, degenerate delta and determinism.
+boundary (96-node block boxes), padding, ragged N, degenerate delta and determinism.
 """
 from __future__ import annotations
 
@@ -120,9 +120,9 @@ def test_max_size_sampled(ser):
     check_nodes(ser, blk, idx=sample(blk.N, 46, seed=7))
 
 
-@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 127, 129, 1000, 3001])
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 95, 96, 97, 127, 129, 383, 384, 385, 1000, 3001])
 def test_ragged_node_counts(ser, n):
-    """Node subsets of the 1/h = 16 sphere: partial 64-node blocks, zero-weight padding in the
+    """Node subsets of the 1/h = 16 sphere: partial 96-node blocks, zero-weight padding in the
     last block, a single node (the self pair only)."""
     blk = config5(inv_h=16)
     idx = np.arange(n) * 7 % blk.N
