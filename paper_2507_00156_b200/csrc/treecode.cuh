@@ -275,6 +275,37 @@ __global__ void __launch_bounds__(256) tree_m2m_kernel(const TreeNode* __restric
   }
 }
 
+#ifndef SER_TREE_ILP2
+#define SER_TREE_ILP2 0  // proxies two at a time into two accumulator sets (tuning macro)
+#endif
+// One target (lane) x one proxy point of an accepted cluster: eq. (31) with the unregularized
+// S, T of eqs. (3)-(4) on the modified weights (the same arithmetic as the pipelined loop below).
+template <int MODE>
+__device__ __forceinline__ void tree_proxy_pair(const double* __restrict__ b, const Tgt& t, Acc& acc) {
+  const double dx = t.y0 - b[0], dy = t.y1 - b[1], dz = t.y2 - b[2];
+  const double ri = rsqrt_nr(fma(dx, dx, fma(dy, dy, dz * dz)));
+  const double ri2 = ri * ri;
+  if (MODE & 1) {
+    const double ux = fma(-t.alpha, b[6], b[3]), uy = fma(-t.alpha, b[7], b[4]), uz = fma(-t.alpha, b[8], b[5]);
+    const double a3 = fma(dx, ux, fma(dy, uy, dz * uz)) * ri2;
+    acc.u0 = fma(fma(dx, a3, ux), ri, acc.u0);
+    acc.u1 = fma(fma(dy, a3, uy), ri, acc.u1);
+    acc.u2 = fma(fma(dz, a3, uz), ri, acc.u2);
+  }
+  if (MODE & 2) {
+    const double* Q = b + 9;
+    const double w0 = fma(Q[0], dx, fma(Q[3], dy, Q[4] * dz));
+    const double w1 = fma(Q[1], dy, Q[5] * dz);
+    const double dQd = fma(dx, w0, fma(dy, w1, dz * (Q[2] * dz)));
+    const double dq0 = fma(dx, t.q0, fma(dy, t.q1, dz * t.q2));
+    const double dn = fma(dx, b[6], fma(dy, b[7], dz * b[8]));
+    const double c = fma(-dq0, dn, dQd) * (ri2 * ri2 * ri);
+    acc.v0 = fma(dx, c, acc.v0);
+    acc.v1 = fma(dy, c, acc.v1);
+    acc.v2 = fma(dz, c, acc.v2);
+  }
+}
+
 struct TreeFarParams {
   const TreeNode* nodes;
   const double* G;        // modified weights
@@ -390,6 +421,20 @@ __global__ void __launch_bounds__(kTreeWarps * 32, SER_TREE_MINB) tree_far_kerne
             for (int c = 0; c < kTreeCh; ++c) sm.buf[lane][3 + c] = Gn[(size_t)k * kTreeCh + c];
           }
           __syncwarp();
+#if SER_TREE_ILP2
+          if (on) {
+            // two proxies per iteration into two accumulator sets: independent chains
+            Acc acc2{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            int j = 0;
+            for (; j + 1 < nk; j += 2) {
+              tree_proxy_pair<MODE>(sm.buf[j], t, acc);
+              tree_proxy_pair<MODE>(sm.buf[j + 1], t, acc2);
+            }
+            if (j < nk) tree_proxy_pair<MODE>(sm.buf[j], t, acc);
+            acc.u0 += acc2.u0; acc.u1 += acc2.u1; acc.u2 += acc2.u2;
+            acc.v0 += acc2.v0; acc.v1 += acc2.v1; acc.v2 += acc2.v2;
+          }
+#else
           if (on) {
             // software pipeline: distance + rsqrt of proxy j+1 overlap the contractions of proxy j
             double gx = t.y0 - sm.buf[0][0], gy = t.y1 - sm.buf[0][1], gz = t.y2 - sm.buf[0][2];
@@ -424,6 +469,7 @@ __global__ void __launch_bounds__(kTreeWarps * 32, SER_TREE_MINB) tree_far_kerne
               gx = nx; gy = ny; gz = nz; gri = nri;
             }
           }
+#endif
         }
       }
       if (dmask) {  // direct far pairs (near pairs masked: K3 owns them)
