@@ -32,7 +32,7 @@ constexpr int kTreeCh = 12;               // fw(3) nw(3) symmetric part of q_a n
 constexpr int kTreeStack = 512;           // DFS stack entries per warp (depth <= 63)
 constexpr int kTreeWarps = 4;             // warps per CTA of tree_far_kernel
 #ifndef SER_TREE_MINB
-#define SER_TREE_MINB 4
+#define SER_TREE_MINB 3  // 12 warps/SM at 168 registers with the two-proxy loop (4: 128 registers, spills)
 #endif
 #ifndef SER_TREE_FUSED_NEAR
 #define SER_TREE_FUSED_NEAR 1  // near units interleaved in the walk kernel's queue (0: separate near_kernel)
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) tree_m2m_kernel(const TreeNode* __restric
 }
 
 #ifndef SER_TREE_ILP2
-#define SER_TREE_ILP2 0  // proxies two at a time into two accumulator sets (tuning macro)
+#define SER_TREE_ILP2 1  // proxies two at a time into two accumulator sets (-3.6% / -1.7% at 1/h = 128 / 256 with MINB 3)
 #endif
 // One target (lane) x one proxy point of an accepted cluster: eq. (31) with the unregularized
 // S, T of eqs. (3)-(4) on the modified weights (the same arithmetic as the pipelined loop below).
