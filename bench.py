@@ -51,7 +51,7 @@ F_NEAR_ISSUED = 331  # ncu-counted FP64 flops per near pair of near_kernel<3> in
 # 1/r^5 3, SL 2 x 24, DL: q_j - q_i 3, d.dq 5, dq/r^5 1 shared + 2 x (d.mw 5, x 1, v += d c 6) = 93,
 # i.e. 46.5 per directed pair (57 when each direction is computed alone).
 F_SYM_UNORDERED_ALG = 93
-F_SYM_UNORDERED_ISSUED = 100  # sym_pair<3>: 61 FP64 instructions = 39 DFMA + 16 DMUL + 6 DADD (2*39 + 16 + 6)
+F_SYM_UNORDERED_ISSUED = 99  # sym_pair<3> (unit-vector form): 60 FP64 instructions = 39 DFMA + 15 DMUL + 6 DADD (2*39 + 15 + 6)
 SMS = 148
 FP64_LANES_PER_SM = 64  # measured: DFMA loop 58.7 FMA/clk/SM at the boost clock (tools/probes)
 

@@ -52,7 +52,10 @@ constexpr int kBlkTileBytes = kSymT * kTileDoubles * 8;    // one R block in SME
 #endif
 constexpr int kSymWarps = SER_SYM_WARPS;                   // I blocks per CTA (one per warp)
 constexpr int kSymThreads = kSymWarps * 32;
-constexpr int kSymStages = 3;                              // R-block TMA ring
+#ifndef SER_SYM_STAGES
+#define SER_SYM_STAGES 3
+#endif
+constexpr int kSymStages = SER_SYM_STAGES;                 // R-block TMA ring
 #ifndef SER_SYM_PIPE
 #define SER_SYM_PIPE 0                                     // software-pipelined step (measured slower)
 #endif
@@ -220,7 +223,8 @@ __device__ __forceinline__ SymNode load_node(const double* __restrict__ t, int l
 //   v_I += T(d) (q_R - q_I) m_R w_R,           v_R += T(-d) (q_I - q_R) m_I w_I
 // with S(d) g = g/r + d (d.g)/r^3 (eq. (3), even in d) and T(d) dq mw =
 // d (d.dq)(d.mw)/r^5 (eq. (4) without the -6, odd in d: the two sign flips of the
-// reverse direction cancel).  61 FP64 instructions for the two directed pairs
+// reverse direction cancel).  61 FP64 instructions for the two directed pairs (60 in the unit-vector
+// form sym_acc_unit below, the default with both layers)
 // (41 for one directed pair in far_pair).  Split in two halves for the software
 // pipeline of sym_kernel: sym_geo (d and the MUFU + Newton 1/r, the long dependency
 // chain) of step k+1 is issued before sym_acc (the contractions) of step k.
@@ -261,9 +265,46 @@ __device__ __forceinline__ void sym_acc(const SymNode& I, const SymNode& R, cons
     ar.v2 = fma(dz, cr, ar.v2);
   }
 }
+#ifndef SER_SYM_DHAT
+#define SER_SYM_DHAT 1  // contractions on the unit vector d/r: 60 FP64 instructions instead of 61 (+1.3% at 1/h = 256)
+#endif
+// The same two directed pairs written on the unit vector e = d/r (3 DMUL): S(d) g = (g + e (e.g))/r and
+// T(d) dq mw = e (e.dq)(e.mw)/r^2, so r^-3 and r^-5 are not formed (one FP64 instruction fewer with both
+// layers; the dots then wait for 1/r).
+template <int MODE>
+__device__ __forceinline__ void sym_acc_unit(const SymNode& I, const SymNode& R, const Geo& g, Acc& ai, Acc& ar) {
+  const double ri = g.ri, ex = g.dx * ri, ey = g.dy * ri, ez = g.dz * ri;
+  if (MODE & 1) {
+    const double gx = fma(-I.alpha, R.mx, R.fx), gy = fma(-I.alpha, R.my, R.fy), gz = fma(-I.alpha, R.mz, R.fz);
+    const double a = fma(ex, gx, fma(ey, gy, ez * gz));
+    ai.u0 = fma(fma(ex, a, gx), ri, ai.u0);
+    ai.u1 = fma(fma(ey, a, gy), ri, ai.u1);
+    ai.u2 = fma(fma(ez, a, gz), ri, ai.u2);
+    const double hx = fma(-R.alpha, I.mx, I.fx), hy = fma(-R.alpha, I.my, I.fy), hz = fma(-R.alpha, I.mz, I.fz);
+    const double b = fma(ex, hx, fma(ey, hy, ez * hz));
+    ar.u0 = fma(fma(ex, b, hx), ri, ar.u0);
+    ar.u1 = fma(fma(ey, b, hy), ri, ar.u1);
+    ar.u2 = fma(fma(ez, b, hz), ri, ar.u2);
+  }
+  if (MODE & 2) {
+    const double qx = R.qx - I.qx, qy = R.qy - I.qy, qz = R.qz - I.qz;
+    const double c = fma(ex, qx, fma(ey, qy, ez * qz)) * (ri * ri);
+    const double ci = c * fma(ex, R.mx, fma(ey, R.my, ez * R.mz));
+    const double cr = c * fma(ex, I.mx, fma(ey, I.my, ez * I.mz));
+    ai.v0 = fma(ex, ci, ai.v0);
+    ai.v1 = fma(ey, ci, ai.v1);
+    ai.v2 = fma(ez, ci, ai.v2);
+    ar.v0 = fma(ex, cr, ar.v0);
+    ar.v1 = fma(ey, cr, ar.v1);
+    ar.v2 = fma(ez, cr, ar.v2);
+  }
+}
 template <int MODE>
 __device__ __forceinline__ void sym_pair(const SymNode& I, const SymNode& R, Acc& ai, Acc& ar) {
-  sym_acc<MODE>(I, R, sym_geo(I, R.x, R.y, R.z), ai, ar);
+  if (SER_SYM_DHAT && MODE == 3)
+    sym_acc_unit<MODE>(I, R, sym_geo(I, R.x, R.y, R.z), ai, ar);
+  else
+    sym_acc<MODE>(I, R, sym_geo(I, R.x, R.y, R.z), ai, ar);
 }
 
 __device__ __forceinline__ void shfl_acc(Acc& a, int src_lane) {
