@@ -618,7 +618,8 @@ NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
   p.nchunks = static_cast<int>(ceil_div(p.nb, p.chunk));
   p.n_items = sym_items(p.nsb, k, p.nchunks);
   p.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kSymGrid, p.n_items)));
-  p.sym_smem = (size_t)kSymStages * kBlkTileBytes + (size_t)kSymWarps * 6 * kBlk * 8 + (size_t)6 * p.chunk * kBlk * 8;
+  p.sym_smem = (size_t)kSymStages * kBlkTileBytes + (size_t)kSymRedBufs * kSymWarps * 6 * kBlk * 8 +
+               (size_t)6 * p.chunk * kBlk * 8;
   p.cub_bytes = cub_sort_bytes(N);
   const int64_t groups = p.Npad / 32;
   p.near_phases = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));

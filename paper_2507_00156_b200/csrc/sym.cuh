@@ -265,6 +265,10 @@ __device__ __forceinline__ void sym_acc(const SymNode& I, const SymNode& R, cons
     ar.v2 = fma(dz, cr, ar.v2);
   }
 }
+#ifndef SER_SYM_RED2
+#define SER_SYM_RED2 1  // double-buffered per-R-block reduction buffer: one CTA barrier per R block (+0.2%)
+#endif
+constexpr int kSymRedBufs = SER_SYM_RED2 ? 2 : 1;
 #ifndef SER_SYM_DHAT
 #define SER_SYM_DHAT 1  // contractions on the unit vector d/r: 60 FP64 instructions instead of 61 (+1.3% at 1/h = 256)
 #endif
@@ -325,14 +329,14 @@ __device__ __forceinline__ int64_t items_before(int64_t c, int k, int nsb) {
   return (int64_t)k * cs * (cs + 1) / 2 + (c - cs) * nsb;
 }
 
-// Dynamic SMEM: R-block ring [kSymStages][2][13][32] | red [kSymWarps][6][64] |
+// Dynamic SMEM: R-block ring [kSymStages][kSymT][32][14] | red [kSymRedBufs][kSymWarps][6][kBlk] |
 // chunk accumulator [6][chunk * 64].
 template <int MODE>
 __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const SymParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
   double* red = ring + kSymStages * kSymT * kTileDoubles;
-  double* cacc = red + kSymWarps * 6 * kBlk;
+  double* cacc = red + kSymRedBufs * kSymWarps * 6 * kBlk;
   __shared__ __align__(8) uint64_t bar[kSymStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
     }
     for (int ri = first; ri < nr; ++ri) {
       const int st = (ri - first) % kSymStages;
+      double* const rd = red + ((ri - first) % kSymRedBufs) * (kSymWarps * 6 * kBlk);
       mbar_wait(&bar[st], (phase_bits >> st) & 1u);
       phase_bits ^= 1u << st;
       const int n = r0 + ri;
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
             for (int t = 0; t < kSymT; ++t) sym_pair<MODE>(I[t], rn, a[t], ra);
             shfl_acc(ra, (lane + 1) & 31);
           }
-          double* rw = red + warp * 6 * kBlk + hf * 32 + lane;
+          double* rw = rd + warp * 6 * kBlk + hf * 32 + lane;
           rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
           rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
         }
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
           sym_acc<MODE>(I1, rn, g1, a1, ra);
           shfl_acc(ra, (lane + 1) & 31);  // lane l holds node (l + kk + 1) & 31 next
           if ((kk & 31) == 31) {          // a half done: lane l holds R node (kk >> 5) * 32 + l
-            double* rw = red + warp * 6 * kBlk + (kk >> 5) * 32 + lane;
+            double* rw = rd + warp * 6 * kBlk + (kk >> 5) * 32 + lane;
             rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
             rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
             ra = Acc{0, 0, 0, 0, 0, 0};
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
           shfl_acc(ra, (lane + 1) & 31);
           shfl_acc(rb, (lane + 1) & 31);
         }
-        double* rw = red + warp * 6 * kBlk + lane;  // lane l holds R nodes l (ra) and 32 + l (rb)
+        double* rw = rd + warp * 6 * kBlk + lane;  // lane l holds R nodes l (ra) and 32 + l (rb)
         rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
         rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
         rw += 32;
@@ -510,14 +515,14 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
             shfl_acc(ra, (lane + 1) & 31);  // lane l holds node (l + kk + 1) & 31 next
           }
           // lane l holds R node hf * 32 + l
-          double* rw = red + warp * 6 * kBlk + hf * 32 + lane;
+          double* rw = rd + warp * 6 * kBlk + hf * 32 + lane;
           rw[0 * kBlk] = ra.u0; rw[1 * kBlk] = ra.u1; rw[2 * kBlk] = ra.u2;
           rw[3 * kBlk] = ra.v0; rw[4 * kBlk] = ra.v1; rw[5 * kBlk] = ra.v2;
         }
        }
 #endif
       } else {  // inactive warp: its share of this R block is zero
-        double* rw = red + warp * 6 * kBlk + lane;
+        double* rw = rd + warp * 6 * kBlk + lane;
 #pragma unroll
         for (int c = 0; c < 6; ++c)
 #pragma unroll
@@ -534,10 +539,10 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
         const int comp = x / kBlk, col = x - comp * kBlk;
         double sum = 0.0;
 #pragma unroll 4
-        for (int w = 0; w < kSymWarps; ++w) sum += red[(w * 6 + comp) * kBlk + col];
+        for (int w = 0; w < kSymWarps; ++w) sum += rd[(w * 6 + comp) * kBlk + col];
         cacc[comp * cw + ri * kBlk + col] += sum;
       }
-      __syncthreads();  // red may be overwritten
+      if (kSymRedBufs == 1) __syncthreads();  // red may be overwritten (with two buffers: the next R block's barrier)
     }
     // flush: the I sums of every warp into this CTA's slice (the chunk's R sums when the chunk changes)
     if (has_i) {
