@@ -575,6 +575,9 @@ __global__ void __launch_bounds__(kSymThreads, SER_SYM_MINB) sym_kernel(const Sy
 // masked (far_pair_masked); near pairs go through the near unit's per-lane queue
 // and near_pair (3 deltas, weights folded).  One unit = (group, phase), phase p
 // takes every phases-th selected sub-tile.
+#ifndef SER_NBR_ILP2
+#define SER_NBR_ILP2 0  // masked far loop of the neighbour units into two accumulator sets (tuning macro)
+#endif
 struct NbrSmem {
   double src[kSrcDoubles][32];
   int q[kQCap][32];
@@ -646,6 +649,9 @@ __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __re
       }
       __syncwarp();
       unsigned smask = 0;
+#if SER_NBR_ILP2
+      Acc fb{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // odd sources: a second, independent accumulation chain
+#endif
 #pragma unroll 2
       for (int kk = 0; kk < 32; ++kk) {
         Src s;
@@ -656,8 +662,16 @@ __device__ __forceinline__ void nbr_unit(const NearParams& p, const double* __re
         const double dx = tg.y0 - s.x, dy = tg.y1 - s.y, dz = tg.y2 - s.z;
         const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
         smask |= (r2 <= p.rc2 ? 1u : 0u) << kk;
+#if SER_NBR_ILP2
+        far_pair_masked<MODE>(s, tg, (kk & 1) ? fb : fa, p.rc2);
+#else
         far_pair_masked<MODE>(s, tg, fa, p.rc2);
+#endif
       }
+#if SER_NBR_ILP2
+      fa.u0 += fb.u0; fa.u1 += fb.u1; fa.u2 += fb.u2;
+      fa.v0 += fb.v0; fa.v1 += fb.v1; fa.v2 += fb.v2;
+#endif
       __syncwarp();
       while (smask) {
         const int bit = __ffs(smask) - 1;
