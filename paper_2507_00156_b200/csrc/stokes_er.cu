@@ -609,7 +609,12 @@ NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
   p.nsb = static_cast<int>(ceil_div(p.nb, kSymWarps));
   // R blocks per item: the largest multiple of the warp count (<= 4 of them, SMEM) that still
   // gives every CTA >= 16 items (balance of the static assignment)
+  auto smem_of = [](int kk) {
+    return (size_t)kSymStages * kBlkTileBytes + (size_t)kSymRedBufs * kSymWarps * 6 * kBlk * 8 +
+           (size_t)6 * kk * kSymWarps * kBlk * 8;
+  };
   int k = SER_SYM_MAXK;
+  while (k > 1 && smem_of(k) > 227 * 1024) --k;  // the opt-in SMEM limit per CTA (tuning macros can exceed it)
   for (; k > 1; --k) {
     const int nch = static_cast<int>(ceil_div(p.nb, k * kSymWarps));
     if (sym_items(p.nsb, k, nch) >= 16 * kSymGrid) break;
@@ -618,8 +623,7 @@ NodePlan make_node_plan(int64_t N, int mode, int phases_override = 0) {
   p.nchunks = static_cast<int>(ceil_div(p.nb, p.chunk));
   p.n_items = sym_items(p.nsb, k, p.nchunks);
   p.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kSymGrid, p.n_items)));
-  p.sym_smem = (size_t)kSymStages * kBlkTileBytes + (size_t)kSymRedBufs * kSymWarps * 6 * kBlk * 8 +
-               (size_t)6 * p.chunk * kBlk * 8;
+  p.sym_smem = smem_of(k);
   p.cub_bytes = cub_sort_bytes(N);
   const int64_t groups = p.Npad / 32;
   p.near_phases = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, ceil_div(10 * 148 * 16, groups))));
