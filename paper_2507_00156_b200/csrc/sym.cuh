@@ -40,11 +40,19 @@ enum NodeField { NX = 0, NY, NZ, NMX, NMY, NMZ, NFX, NFY, NFZ, NQX, NQY, NQZ, NA
 constexpr int kNodeStride = SER_SYM_AOS ? 14 : kNodeFields;       // doubles per node in a tile
 constexpr int kTileDoubles = 32 * kNodeStride;                     // one 32-node tile
 __host__ __device__ constexpr int nfield(int l, int f) { return SER_SYM_AOS ? l * 14 + f : f * 32 + l; }
+#ifndef SER_SYM_PIPE
+#define SER_SYM_PIPE 0                                     // software-pipelined step (measured slower)
+#endif
+#ifndef SER_SYM_TR2
+#define SER_SYM_TR2 0                                      // 2 R nodes per step (4 pairs): tuning macro
+#endif
 #ifndef SER_SYM_T
 #define SER_SYM_T 3                                        // I nodes per lane = 32-node sub-tiles per block
                                                            // (3 at 8 warps: +2.9% over 2 at 12 warps; 4: -3%)
 #endif
 constexpr int kSymT = SER_SYM_T;
+static_assert(kSymT >= 2 && kSymT <= 4, "I nodes per lane: 2, 3 or 4 (registers)");
+static_assert(kSymT == 2 || !(SER_SYM_PIPE || SER_SYM_TR2), "the pipelined and two-R-node steps are written for T = 2");
 constexpr int kBlk = 32 * kSymT;                           // nodes per symmetric block (96: 3 sub-tiles)
 constexpr int kBlkTileBytes = kSymT * kTileDoubles * 8;    // one R block in SMEM (TMA unit)
 #ifndef SER_SYM_WARPS
@@ -56,12 +64,6 @@ constexpr int kSymThreads = kSymWarps * 32;
 #define SER_SYM_STAGES 3
 #endif
 constexpr int kSymStages = SER_SYM_STAGES;                 // R-block TMA ring
-#ifndef SER_SYM_PIPE
-#define SER_SYM_PIPE 0                                     // software-pipelined step (measured slower)
-#endif
-#ifndef SER_SYM_TR2
-#define SER_SYM_TR2 0                                      // 2 R nodes per step (4 pairs): tuning macro
-#endif
 #ifndef SER_SYM_UNROLL
 #define SER_SYM_UNROLL 8                                   // steps per loop iteration (8: +0.6% over 4; 2, 1: -1%)
 #endif
