@@ -224,7 +224,7 @@ int stokes_er_eval_ex(const double* src_xyz, const double* src_normal, const dou
  * the pair_kernel events bracket the symmetric far kernel, the near_kernel
  * events the neighbour kernel (near pairs + the far pairs of the blocks the
  * symmetric kernel leaves out); near_phases is honoured; stats[0..3] = items,
- * CTAs, R blocks per item, 2.
+ * CTAs, R blocks per item, I nodes per lane (3).
  */
 size_t stokes_er_nodes_workspace_bytes(int64_t N, int mode);
 size_t stokes_er_nodes_workspace_bytes_ex(int64_t N, int mode, const stokes_er_options* options);

@@ -749,7 +749,7 @@ int run_nodes(const double* sx, const double* sn, const double* sw, const double
     opt->stats[0] = P.n_items;
     opt->stats[1] = P.G;
     opt->stats[2] = P.chunk;
-    opt->stats[3] = 2;
+    opt->stats[3] = kSymT;  // I nodes per lane of the symmetric kernel
   }
   finalize_nodes<MODE><<<ceil_div(N, 256), 256, 0, s>>>(pacc, P.G, near_out, P.near_phases, tgt, orig, N, P.Npad,
                                                          ishard == 0 ? 0.5 : 0.0, out_u, out_v);
