@@ -175,10 +175,16 @@ def test_self_convergence_golden():
     g = json.load(open(path))
     e = {int(k): v for k, v in g["max_err"].items()}
     l2 = {int(k): v for k, v in g["l2_err"].items()}
-    assert 1e-3 <= e[16] <= 1e-2                 # Table 2: 3.17e-3
-    assert 3e-5 <= l2[16] <= 1e-3                # Table 2: 1.19e-4
+    # Table 2 prints 3.17e-3 / 1.19e-4 at 1/h = 16 from a treecode run with an
+    # unstated interpolation (R20); the direct-sum oracle must land within a factor
+    # 1.5 (max) and 2 (L2) of them -- measured 1.28x and 1.79x
+    assert 3.17e-3 / 1.5 <= e[16] <= 3.17e-3 * 1.5
+    assert 1.19e-4 / 2.0 <= l2[16] <= 1.19e-4 * 2.0
     assert l2[8] / l2[16] > 2.0 ** 3.5           # high order in L2 (the max sits at the contact node)
-    assert all(12 <= it <= 14 for k, it in g["iterations"].items() if int(k) >= 16)
+    paper_iters = {16: 13, 32: 12}               # Table 2's GMRES iteration counts (tol 1e-10)
+    for k, it in g["iterations"].items():
+        if int(k) in paper_iters:
+            assert abs(it - paper_iters[int(k)]) <= 1, (k, it)
 
 
 def test_match_nodes_nested():
