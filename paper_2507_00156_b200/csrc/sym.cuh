@@ -71,6 +71,9 @@ constexpr int kSymUnroll = SER_SYM_UNROLL;
 #ifndef SER_SYM_MINB
 #define SER_SYM_MINB 1                                     // resident CTAs per SM (tuning macro)
 #endif
+#ifndef SER_SYM_RSQ2
+#define SER_SYM_RSQ2 0                                     // quadratic Newton rsqrt in sym_geo (tuning macro)
+#endif
 #ifndef SER_SYM_MAXK
 #define SER_SYM_MAXK 3                                     // R blocks per item <= MAXK * warps (SMEM)
 #endif
@@ -235,7 +238,16 @@ __device__ __forceinline__ Geo sym_geo(const SymNode& I, double rx, double ry, d
   g.dx = I.x - rx;
   g.dy = I.y - ry;
   g.dz = I.z - rz;
+#if SER_SYM_RSQ2
+  // tuning variant: one quadratic Newton step from the MUFU seed (4 FP64 instructions instead of 5;
+  // accurate only if the seed is; tools/probes/rsqrt_seed_probe.cu)
+  const double x = fma(g.dx, g.dx, fma(g.dy, g.dy, g.dz * g.dz));
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  g.ri = fma(y * 0.5, fma(-x, y * y, 1.0), y);
+#else
   g.ri = rsqrt_nr(fma(g.dx, g.dx, fma(g.dy, g.dy, g.dz * g.dz)));
+#endif
   return g;
 }
 template <int MODE>
