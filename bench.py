@@ -294,8 +294,13 @@ def run_tree(args, rank, world):
     import oracle
     rng = np.random.default_rng(0)
     idx = rng.choice(M, min(M, 128), replace=False)
-    _, _, st = oracle.evaluate_tree_block(block.take_targets(idx), leaf_size=tp[0], degree=tp[1], theta=tp[2],
-                                          stats=True)
+    ut, vt, st = oracle.evaluate_tree_block(block.take_targets(idx), leaf_size=tp[0], degree=tp[1], theta=tp[2],
+                                            stats=True)
+    ug, vg = u.cpu().numpy()[:, idx], v.cpu().numpy()[:, idx]
+    parity = {"u_max_rel": float(np.abs(ug - ut).max() / np.abs(ut).max()),
+              "v_max_rel": float(np.abs(vg - vt).max() / np.abs(vt).max()), "targets_sampled": int(len(idx)),
+              "sample_seed": 0, "reference": "oracle treecode (oracle_eval_tree, same N0, p, theta), same seeded inputs",
+              "tolerance": 1e-12}
     proxies = st[1] / len(idx) * (tp[1] + 1) ** 3 * M
     direct = st[2] / len(idx) * M
     near = near_pair_count(block)
@@ -318,7 +323,7 @@ def run_tree(args, rank, world):
                                    f"{F_PROXY_ALG} flops per target-proxy interaction, {F_FAR_ALG} per direct far "
                                    f"pair, {F_NEAR_ALG} per near pair",
                          "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk/SM x 2 x 1965 MHz"},
-            "clocks": clk.summary(), "gpu_launches": K * 9,
+            "clocks": clk.summary(), "parity": parity, "gpu_launches": K * 9,
             "gpu_launches_note": "per step: bbox, morton, pack sources, pack targets, P2M, M2M per level (<= 3), "
                                  "tree walk + near units, finalize (+ CUB sort)",
             "e2e": None}
@@ -480,6 +485,12 @@ def run_config4(args, rank, world):
             "gpu_launches_note": "per block: bbox, 2 morton, pack sources, pack targets, fused far+near, finalize "
                                  "(+ CUB sort)",
             "e2e": None}
+    # sampled parity of each block's output (after the timed region) against the oracle's definition mode
+    recs = [sampled_parity(b, u.cpu().numpy(), v.cpu().numpy(), n=16)[0] for b, (u, v) in zip(blocks, outs)]
+    line["parity"] = {"u_max_rel": max(r["u_max_rel"] for r in recs), "v_max_rel": max(r["v_max_rel"] for r in recs),
+                      "targets_sampled": sum(r["targets_sampled"] for r in recs), "sample_seed": recs[0]["sample_seed"],
+                      "reference": recs[0]["reference"] + " (16 targets per block, max over the 4 blocks)",
+                      "tolerance": recs[0]["tolerance"]}
     if not args.no_cpu_baseline:
         import oracle
         rng = np.random.default_rng(0)
