@@ -414,6 +414,11 @@ def run_onsurface(args, rank, world):
         uu, vv = u.cpu().numpy()[:, idx], v.cpu().numpy()[:, idx]
         line["config"]["max_rel_diff_vs_oracle_sample"] = max(float(np.abs(uu - ur).max() / np.abs(ur).max()),
                                                               float(np.abs(vv - vr).max() / np.abs(vr).max()))
+        line["parity"] = {"u_max_rel": float(np.abs(uu - ur).max() / np.abs(ur).max()),
+                          "v_max_rel": float(np.abs(vv - vr).max() / np.abs(vr).max()),
+                          "targets_sampled": int(len(idx)), "sample_seed": 0,
+                          "reference": "oracle s# mode (oracle_eval_sharp, cutoff 7), same seeded inputs",
+                          "tolerance": 1e-12}
         line["cpu_baseline"] = {"value": len(idx) * N / dt, "unit": UNIT, "cores": oracle.max_threads(),
                                 "kind": "oracle",
                                 "sample": f"{len(idx)} random targets of {M} x all {N} sources, sharp mode, "
@@ -597,6 +602,12 @@ def run_twodrop(args, rank, world):
         o.apply(vec)
         dt = time.perf_counter() - t0
         Ns = [d.N for d in tds.drops]
+        # parity of the operator (the solve's only kernel path) on the same small instance and vector
+        got = ser.twodrop_solver(tds, device=dev).apply(torch.from_numpy(vec).to(dev)).cpu().numpy()
+        ref = o.apply(vec)
+        parity = {"apply_max_rel": float(np.abs(got - ref).max() / np.abs(ref).max()),
+                  "instance": f"1/h = {min(args.inv_h, 16)}, seeded vector U[-1,1]",
+                  "reference": "oracle/twodrop.py operator application (localized mode)", "tolerance": 1e-12}
         cpu = {"value": sum(Ns[i] * Ns[j] for i in range(2) for j in range(2)) / dt, "unit": UNIT,
                "cores": __import__("oracle").max_threads(), "kind": "oracle",
                "sample": f"one operator application (4 blocks) of the oracle at 1/h = {min(args.inv_h, 16)} "
@@ -627,6 +638,7 @@ def run_twodrop(args, rank, world):
                     "note": "host arrays -> device, stencil setup, solve, u -> host"}}
     if cpu:
         line["cpu_baseline"] = cpu
+        line["parity"] = parity
     if dist is not None:
         dist.destroy_process_group()
     return line
