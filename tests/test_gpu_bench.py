@@ -48,3 +48,5 @@ def test_bench_other_workloads(args):
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [json.loads(s) for s in r.stdout.splitlines() if s.startswith("{")]
     assert len(lines) == 1 and lines[0]["value"] > 0 and 0 < lines[0]["roofline"]["frac"] < 1
+    par = lines[0]["parity"]  # every line carries its sampled oracle parity
+    assert par["targets_sampled"] > 0 and max(par["u_max_rel"], par["v_max_rel"]) <= par["tolerance"] == 1e-12
